@@ -1,0 +1,290 @@
+"""Native implementations behind recognised kernels.
+
+``build()`` type-checks a kernel and looks its canonical form up here
+(kernel/canon.py).  Each binding launches one hand-written sm_100a kernel of
+libofl.so with the exact semantics of the reference's sequential executor
+(/root/reference/pkg/src/offloadrt/kernel/codegen.py:107-128): work items
+gtid = 0 .. grid*block-1 each run the body.  Items are independent in every
+bound kernel, so the device order is free.
+
+Host-side pre-checks reproduce the executor's kernel aborts: the first
+out-of-bounds buffer index (in gtid order, store index before loads as the
+executor evaluates them) fails the token with OobAccessError carrying that
+index.  Unlike the sequential executor no partial writes happen before the
+abort — the kernel is not launched at all.
+
+Builtin programs (``BUILTIN_KERNELS``) extend the language's reach where the
+reference has no way to express the workload: fp32 data (the language has no
+f32, /root/reference/pkg/src/offloadrt/kernel/lang.py:29) and the multi-step
+heat equation with temporal blocking.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from functools import lru_cache
+from typing import Callable, Optional
+
+from . import _native
+from .errors import BadArgsError, OobAccessError
+from .kernel import parse_and_validate
+from .kernel.canon import canonical
+
+M32 = 0xFFFFFFFF
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@dataclass(frozen=True)
+class Binding:
+    name: str
+    kinds: tuple  # parameter kinds, in order
+    # launch(stream, values, items, ticket_ref) -> status, or raises
+    launch: Callable
+    # first out-of-bounds index (or None) given values and items
+    oob: Optional[Callable] = None
+
+
+def _first_oob(candidates, failing) -> Optional[int]:
+    """Smallest gtid among candidates whose accesses fail; returns the failing
+    index reported for it."""
+    for g in sorted(set(c for c in candidates if c is not None and c >= 0)):
+        idx = failing(g)
+        if idx is not None:
+            return idx
+    return None
+
+
+# -- STREAM ----------------------------------------------------------------------
+
+
+def _stream_binding(name: str, op: int, kinds: tuple) -> Binding:
+    has_c = op in (_native.STREAM_ADD, _native.STREAM_TRIAD)
+    has_s = op in (_native.STREAM_SCALE, _native.STREAM_TRIAD)
+
+    def unpack(v):
+        a, b = v[0], v[1]
+        c = v[2] if has_c else None
+        s = v[3] if op == _native.STREAM_TRIAD else (v[2] if has_s else 0.0)
+        n = v[-1]
+        return a, b, c, s, n
+
+    def oob(v, items):
+        a, b, c, _, n = unpack(v)
+        m = min(n, items)
+        lens = [a.elements("buffer_f64"), b.elements("buffer_f64")]
+        if c is not None:
+            lens.append(c.elements("buffer_f64"))
+        lo = min(lens)
+        return lo if m > lo else None
+
+    def launch(st, v, items, ticket):
+        a, b, c, s, n = unpack(v)
+        m = min(n, items)
+        return st.lib.ofl_stream_op(
+            st.ptr, op, a.ptr, b.ptr, c.ptr if c is not None else b.ptr, float(s), m, ticket
+        )
+
+    return Binding(name, kinds, launch, oob)
+
+
+# -- stencil ---------------------------------------------------------------------
+
+
+def _stencil_oob(v, items):
+    x, y, n = v
+    m = min(n, items)
+    if m == 0:
+        return None
+    lx, ly = x.elements("buffer_f64"), y.elements("buffer_f64")
+
+    def failing(g):
+        if g >= m:
+            return None
+        if g >= ly:
+            return g  # store index is checked first
+        if g == 0 or g == ((n - 1) & M32):
+            return g if g >= lx else None
+        for idx in (g - 1, g, g + 1):
+            if idx >= lx:
+                return idx
+        return None
+
+    return _first_oob([0, 1, lx - 1, lx, ly, m - 1], failing)
+
+
+def _stencil_launch(st, v, items, ticket):
+    x, y, n = v
+    m = min(n, items)
+    if m and x is y:
+        raise BadArgsError(
+            "stencil: in-place update (x is y) is order-dependent; use two buffers"
+        )
+    return st.lib.ofl_stencil(st.ptr, x.ptr, y.ptr, n, m, ticket)
+
+
+# -- mandelbrot ------------------------------------------------------------------
+
+
+def _mandel_oob(v, items):
+    out, width, height = v[0], v[1], v[2]
+    total = (width * height) & M32
+    m = min(total, items)
+    lo = out.elements("buffer_u32")
+    return lo if m > lo else None
+
+
+def _mandel_launch(st, v, items, ticket):
+    out, width, height, re0, re1, im0, im1, esc, max_iter = v
+    return st.lib.ofl_mandelbrot(
+        st.ptr, out.ptr, width, height, float(re0), float(re1), float(im0), float(im1),
+        float(esc), max_iter, items, 0, 1, ticket,
+    )
+
+
+# -- sum -------------------------------------------------------------------------
+
+
+def _sum_oob(v, items):
+    inp, res, n = v
+    if n > inp.elements("buffer_u32"):
+        return inp.elements("buffer_u32")
+    if res.elements("buffer_u32") < 1:
+        return 0
+    return None
+
+
+def _sum_launch(st, v, items, ticket):
+    inp, res, n = v
+    return st.lib.ofl_sum_u32(st.ptr, inp.ptr, res.ptr, n, ticket)
+
+
+# -- partition -------------------------------------------------------------------
+
+
+def _partition_oob(v, items):
+    out, offset, count = v
+    m = min(count, items)
+    lo = out.elements("buffer_f64")
+    return lo if m > lo else None
+
+
+def _partition_launch(st, v, items, ticket):
+    out, offset, count = v
+    return st.lib.ofl_partition(st.ptr, out.ptr, offset, min(count, items), ticket)
+
+
+# -- builtins (no .k form) -------------------------------------------------------
+
+
+def _dot_oob(v, items):
+    a, b, out, n = v
+    m = min(n, items)
+    lo = min(a.elements("buffer_f32"), b.elements("buffer_f32"))
+    if m > lo:
+        return lo
+    if out.elements("buffer_f64") < 1:
+        return 0
+    return None
+
+
+def _dot_launch(st, v, items, ticket):
+    a, b, out, n = v
+    return st.lib.ofl_dot_f32(st.ptr, a.ptr, b.ptr, out.ptr, min(n, items), ticket)
+
+
+def heat_block() -> int:
+    """Steps fused per HBM pass by the heat builtin (OFL_HEAT_TB, default 8)."""
+    return max(1, min(64, int(os.environ.get("OFL_HEAT_TB", "8"))))
+
+
+def _heat_oob(v, items):
+    x, y, n, steps = v
+    lo = min(x.elements("buffer_f64"), y.elements("buffer_f64"))
+    return lo if n > lo else None
+
+
+def _heat_launch(st, v, items, ticket):
+    x, y, n, steps = v
+    if items < n:
+        raise BadArgsError("heat: the launch must cover all n cells")
+    if x is y:
+        raise BadArgsError("heat: x and y must be distinct buffers")
+    if n == 0 or steps == 0:
+        return st.lib.ofl_d2d(st.ptr, x.ptr, x.ptr, 0, ticket)
+    return st.lib.ofl_heat(st.ptr, x.ptr, y.ptr, n, steps, heat_block(), ticket)
+
+
+BUILTIN_KERNELS = {
+    # fp32 dot product with fp64 accumulation into out[0]
+    "dot_f32": Binding(
+        "dot_f32", ("buffer_f32", "buffer_f32", "buffer_f64", "scalar_u32"), _dot_launch, _dot_oob
+    ),
+    # `steps` applications of stencil.k, ping-ponging x <-> y; the result is
+    # in x for even steps, in y for odd steps
+    "heat": Binding(
+        "heat", ("buffer_f64", "buffer_f64", "scalar_u32", "scalar_u32"), _heat_launch, _heat_oob
+    ),
+}
+
+BUILTIN_PARAM_NAMES = {
+    "dot_f32": ("a", "b", "out", "n"),
+    "heat": ("x", "y", "n", "steps"),
+}
+
+
+# -- canonical-form table --------------------------------------------------------
+
+
+def _source(name: str) -> str:
+    with open(os.path.join(_HERE, "kernels", f"{name}.k"), encoding="utf-8") as fh:
+        return fh.read()
+
+
+def kernel_source(name: str) -> str:
+    """Source text of a bundled kernel program (stream, stencil, mandelbrot,
+    sum, partition)."""
+    return _source(name)
+
+
+@lru_cache(maxsize=None)
+def _table() -> dict:
+    specs = {
+        ("stream", "copy"): lambda k: _stream_binding("copy", _native.STREAM_COPY, k),
+        ("stream", "scale"): lambda k: _stream_binding("scale", _native.STREAM_SCALE, k),
+        ("stream", "add"): lambda k: _stream_binding("add", _native.STREAM_ADD, k),
+        ("stream", "triad"): lambda k: _stream_binding("triad", _native.STREAM_TRIAD, k),
+        ("stencil", "stencil"): lambda k: Binding("stencil", k, _stencil_launch, _stencil_oob),
+        ("mandelbrot", "mandelbrot"): lambda k: Binding("mandelbrot", k, _mandel_launch, _mandel_oob),
+        ("sum", "sum"): lambda k: Binding("sum", k, _sum_launch, _sum_oob),
+        ("partition", "partition"): lambda k: Binding(
+            "partition", k, _partition_launch, _partition_oob
+        ),
+    }
+    table = {}
+    parsed: dict = {}
+    for (src, kname), make in specs.items():
+        if src not in parsed:
+            parsed[src] = parse_and_validate(_source(src))
+        ir = parsed[src][kname]
+        form = canonical(ir)
+        table[form] = make(form[0])
+    return table
+
+
+def lookup(ir) -> Optional[Binding]:
+    return _table().get(canonical(ir))
+
+
+def check_oob(binding: Binding, values: list, items: int) -> Optional[OobAccessError]:
+    if binding.oob is None:
+        return None
+    idx = binding.oob(values, items)
+    if idx is None:
+        return None
+    return OobAccessError(f"kernel buffer index {idx} out of range")
+
+
+def new_ticket():
+    return ctypes.c_uint64()

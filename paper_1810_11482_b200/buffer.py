@@ -1,0 +1,195 @@
+"""Device-resident buffers.
+
+Replaces the reference BufferObject (/root/reference/pkg/src/offloadrt/
+buffer.py:22-66): untyped bytes, zero-initialised at creation, every access
+bounds-checked against [0, size).  The bytes live in HBM (cudaMalloc); writes
+and reads are stream-ordered cudaMemcpyAsync (see hostmem.py for the host
+side of each copy); kernels see typed views by pointer + element count.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+from . import hostmem
+from .completion import DeviceToken
+from .device import DeviceObject
+from .errors import BadArgsError, OobAccessError
+from .futures import CompletionToken, make_ready
+
+ELEM_SIZE = {"buffer_f64": 8, "buffer_u32": 4, "buffer_f32": 4}
+
+
+def check_range(offset: int, size: int, total: int, what: str) -> None:
+    if offset < 0 or size < 0:
+        raise BadArgsError(f"{what}: negative offset or size")
+    if offset + size > total:
+        raise OobAccessError(
+            f"{what}: range [{offset}, {offset + size}) exceeds buffer of {total} bytes"
+        )
+
+
+class BufferObject:
+    """Owning-side buffer: a device allocation and the device whose streams
+    order access to it."""
+
+    __slots__ = ("device", "size_bytes", "ptr", "__weakref__")
+
+    def __init__(self, device: DeviceObject, size_bytes: int):
+        if size_bytes <= 0:
+            raise BadArgsError("buffer size must be positive")
+        self.device = device
+        self.size_bytes = size_bytes
+        self.ptr = 0
+        self.ptr = device.allocate(size_bytes)
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                self.device.release(self.ptr, self.size_bytes)
+            except Exception:  # noqa: BLE001 - interpreter teardown
+                pass
+            self.ptr = 0
+
+    def elements(self, kind: str) -> int:
+        """Element count of the typed view; a tail shorter than one element
+        is unaddressable (reference buffer.py:57-66)."""
+        try:
+            return self.size_bytes // ELEM_SIZE[kind]
+        except KeyError:
+            raise BadArgsError(f"not a buffer kind: {kind}") from None
+
+    # -- copies ------------------------------------------------------------------
+    def enqueue_write(self, offset: int, data, stream: int = 0) -> CompletionToken:
+        addr, n, owner = hostmem.host_view(data)
+        check_range(offset, n, self.size_bytes, "write")
+        st = self.device.stream(stream)
+        lib = st.lib
+        ticket = ctypes.c_uint64()
+        dst = self.ptr + offset
+        if n == 0 or hostmem.is_pinned(addr, n):
+            status = lib.ofl_h2d(st.ptr, dst, addr, n, ctypes.byref(ticket))
+            if status:
+                raise_status(status, "write")
+            if n:
+                st.keep(ticket.value, owner)
+        elif n <= hostmem.SMALL_PAGEABLE:
+            # the driver stages pageable data before returning
+            status = lib.ofl_h2d(st.ptr, dst, addr, n, ctypes.byref(ticket))
+            if status:
+                raise_status(status, "write")
+        else:
+            block = hostmem.pool.get(n)
+            hostmem.memcpy(block.addr, addr, n)
+            status = lib.ofl_h2d(st.ptr, dst, block.addr, n, ctypes.byref(ticket))
+            if status:
+                hostmem.pool.put(block)
+                raise_status(status, "write")
+            hostmem.free_block_later(st, ticket.value, block)
+        return DeviceToken(st, ticket.value)
+
+    def enqueue_read(self, offset: int, size: int, stream: int = 0) -> CompletionToken:
+        """Token for the bytes of [offset, offset+size) at this stream position."""
+        check_range(offset, size, self.size_bytes, "read")
+        if size == 0:
+            return make_ready(b"")
+        st = self.device.stream(stream)
+        block = hostmem.pool.get(size)
+        ticket = ctypes.c_uint64()
+        status = st.lib.ofl_d2h(st.ptr, block.addr, self.ptr + offset, size, ctypes.byref(ticket))
+        if status:
+            hostmem.pool.put(block)
+            raise_status(status, "read")
+        landing = _Landing(block, size)
+        tok = DeviceToken(st, ticket.value, landing.take)
+        # the block goes back to the pool only after the copy completed and
+        # its bytes were taken (or the token was dropped unobserved)
+        st.keep(ticket.value, landing.release_later)
+        return tok
+
+    def enqueue_read_into(self, offset: int, out, stream: int = 0) -> CompletionToken:
+        """Copy [offset, offset+len(out)) into the writable host buffer `out`
+        at this stream position.  Zero-copy when `out` is pinned
+        (hostmem.pinned_empty).  The token's value is `out`."""
+        addr, n, owner = hostmem.writable_view(out)
+        check_range(offset, n, self.size_bytes, "read")
+        st = self.device.stream(stream)
+        ticket = ctypes.c_uint64()
+        if n == 0:
+            return make_ready(out)
+        if hostmem.is_pinned(addr, n):
+            status = st.lib.ofl_d2h(st.ptr, addr, self.ptr + offset, n, ctypes.byref(ticket))
+            if status:
+                raise_status(status, "read")
+            st.keep(ticket.value, owner)
+            return DeviceToken(st, ticket.value, lambda: out)
+        block = hostmem.pool.get(n)
+        status = st.lib.ofl_d2h(st.ptr, block.addr, self.ptr + offset, n, ctypes.byref(ticket))
+        if status:
+            hostmem.pool.put(block)
+            raise_status(status, "read")
+        landing = _Landing(block, n, into=addr, keep=owner)
+        st.keep(ticket.value, landing.release_later)
+        return DeviceToken(st, ticket.value, lambda: (landing.take(), out)[1])
+
+
+class _Landing:
+    """A staging block receiving a device->host copy.  `take` (after
+    completion) extracts the data; the block is recycled once both the copy
+    is complete (stream purge) and the data has been taken."""
+
+    __slots__ = ("block", "size", "into", "keep_obj", "data", "taken", "purged", "lock")
+
+    def __init__(self, block, size: int, into: int = 0, keep=None):
+        self.lock = threading.Lock()
+        self.block = block
+        self.size = size
+        self.into = into
+        self.keep_obj = keep
+        self.data = None
+        self.taken = False
+        self.purged = False
+
+    def _extract(self):
+        if self.into:
+            hostmem.memcpy(self.into, self.block.addr, self.size)
+            return None
+        return bytes(self.block.array[: self.size])
+
+    def take(self):
+        with self.lock:
+            if not self.taken:
+                self.data = self._extract()
+                self.taken = True
+            if self.purged:
+                self._recycle()
+            data, self.data = self.data, None
+        return data
+
+    def release_later(self):
+        # copy is complete; if nobody took the data yet, keep the block until
+        # they do (the token holds this landing through its finish function)
+        with self.lock:
+            self.purged = True
+            if self.taken:
+                self._recycle()
+
+    def _recycle(self):
+        if self.block is not None:
+            hostmem.pool.put(self.block)
+            self.block = None
+
+    def __del__(self):
+        # token dropped unobserved after the copy completed
+        if self.block is not None and self.purged:
+            try:
+                hostmem.pool.put(self.block)
+            except Exception:  # noqa: BLE001
+                pass
+
+
+def raise_status(status: int, what: str):
+    from . import _native
+
+    raise _native.error_for(status, what)

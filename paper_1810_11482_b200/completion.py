@@ -1,0 +1,168 @@
+"""Tokens for stream-ordered device operations, and the completion thread.
+
+Replaces the reference's per-stream worker threads that fulfil promises
+after running each operation (/root/reference/pkg/src/offloadrt/device.py:
+129-157, futures.py:76-89).  Here the device runs the operation; the token
+only records *where* on which stream it sits (a ticket, include/ofl.h), and
+completion is observed on demand:
+
+* ``done()``  -> ``ofl_query``  (cudaEventQuery on a lazily placed marker)
+* ``get()``   -> ``ofl_wait``   (cudaEventSynchronize; no thread handoff)
+* ``then()``  -> ``ofl_notify`` (cudaLaunchHostFunc pushes the token id into
+  a queue and signals an eventfd; one completion thread blocked in
+  ``os.read`` drains ids in batches and fulfils the tokens — no polling)
+
+A token may carry a ``finish`` function run exactly once when the operation
+is known complete (e.g. turning a pinned staging block into the ``bytes``
+the reference's ``enqueue_read`` returns); an exception from it fails the
+token, which is how host-side post-conditions surface.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+import threading
+from typing import Any, Callable, Optional
+
+from . import _native
+from .errors import InternalError
+from .futures import _PENDING, CompletionToken, _lock
+
+_ids = itertools.count(1)
+_pending: dict[int, "DeviceToken"] = {}
+_pending_lock = threading.Lock()
+_thread: Optional[threading.Thread] = None
+_thread_lock = threading.Lock()
+
+
+def _completion_loop(fd: int) -> None:
+    lib = _native.load()
+    cap = 1024
+    buf = (ctypes.c_uint64 * cap)()
+    count = ctypes.c_int(0)
+    while True:
+        try:
+            os.read(fd, 8)
+        except InterruptedError:
+            continue
+        while True:
+            lib.ofl_drain(buf, cap, ctypes.byref(count))
+            n = count.value
+            if n == 0:
+                break
+            with _pending_lock:
+                toks = [_pending.pop(buf[i], None) for i in range(n)]
+            for tok in toks:
+                if tok is not None:
+                    tok._finish_now()
+
+
+def _ensure_thread() -> None:
+    global _thread
+    if _thread is not None:
+        return
+    with _thread_lock:
+        if _thread is None:
+            fd = _native.load().ofl_completion_fd()
+            if fd < 0:
+                raise InternalError("completion eventfd unavailable")
+            t = threading.Thread(
+                target=_completion_loop, args=(fd,), name="ofl-completion", daemon=True
+            )
+            t.start()
+            _thread = t
+
+
+class DeviceToken(CompletionToken):
+    """Token of one stream-ordered operation: (stream, ticket)."""
+
+    __slots__ = ("_stream", "_ticket", "_finish", "_claimed")
+
+    def __init__(self, stream, ticket: int, finish: Optional[Callable[[], Any]] = None):
+        super().__init__()
+        self._stream = stream
+        self._ticket = ticket
+        self._finish = finish
+        self._claimed = False
+
+    def _finish_now(self) -> None:
+        """The operation is complete on the device: produce the value.
+        Exactly one caller runs ``finish``; the others return at once."""
+        with _lock:
+            if self._state != _PENDING or self._claimed:
+                return
+            self._claimed = True
+            fin = self._finish
+            self._finish = None
+        if fin is None:
+            self._try_complete(value=None)
+            return
+        try:
+            value = fin()
+        except BaseException as exc:  # noqa: BLE001 - delivered through the token
+            self._try_complete(error=exc)
+            return
+        self._try_complete(value=value)
+
+    def _fail(self, status: int, what: str) -> None:
+        with _lock:
+            if self._claimed:
+                return
+            self._claimed = True
+            self._finish = None
+        self._try_complete(error=_native.error_for(status, what))
+
+    def _poll(self) -> bool:
+        if self._state != _PENDING:
+            return True
+        s = self._stream
+        if s.done_ticket() < self._ticket:
+            ready = ctypes.c_int(0)
+            status = s.lib.ofl_query(s.ptr, self._ticket, ctypes.byref(ready))
+            if status:
+                self._fail(status, "device operation failed")
+                return True
+            if not ready.value:
+                return False
+        self._finish_now()
+        return self._state != _PENDING
+
+    def _block(self, timeout: Optional[float]) -> bool:
+        if self._state != _PENDING:
+            return True
+        if timeout is not None:
+            return super()._block(timeout)
+        s = self._stream
+        status = s.lib.ofl_wait(s.ptr, self._ticket)
+        if status:
+            self._fail(status, "device operation failed")
+        else:
+            self._finish_now()
+        if self._state == _PENDING:  # another thread is running finish()
+            self._wait_quiet(None)
+        return True
+
+    def _arm(self) -> None:
+        _ensure_thread()
+        tid = next(_ids)
+        with _pending_lock:
+            _pending[tid] = self
+        s = self._stream
+        status = s.lib.ofl_notify(s.ptr, self._ticket, tid)
+        if status:
+            with _pending_lock:
+                _pending.pop(tid, None)
+            self._fail(status, "completion notify failed")
+
+
+def wake(token: CompletionToken) -> None:
+    """Deliver a host-side token through the completion thread (used when a
+    continuation must not run on the caller's stack)."""
+    if isinstance(token, DeviceToken):
+        _ensure_thread()
+        tid = next(_ids)
+        with _pending_lock:
+            _pending[tid] = token
+        _native.load().ofl_completion_post(tid)

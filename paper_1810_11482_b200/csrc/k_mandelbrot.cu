@@ -1,0 +1,137 @@
+// Escape-time Mandelbrot (mandelbrot.k, /root/reference/pkg/src/offloadrt/
+// bench/kernels/mandelbrot.k:6-29; validator harness.py:133-158).
+//
+// Per pixel gtid < total = (width*height) mod 2^32:
+//   px = gtid mod width, py = gtid / width
+//   cre = re0 + ((f64(px) + 0.5) * (re1 - re0)) / f64(width)
+//   cim = im0 + ((f64(py) + 0.5) * (im1 - im0)) / f64(height)
+//   repeat max_iter times: break if zr*zr + zi*zi > esc (checked BEFORE the
+//   increment); t = (zr*zr - zi*zi) + cre; zi = (2*zr)*zi + cim; zr = t; ++count
+// Every operation is a separate round-to-nearest IEEE op (no FMA), so the
+// counts are bit-identical to the reference's CPU executor.
+//
+// FP64-issue bound.  Divergence: a warp works on a compact 8x4 pixel tile
+// (neighbouring pixels escape at similar counts), and warps pull units of
+// kTilesPerUnit tiles from an atomic queue so the slow (bounded) regions do
+// not leave SMs idle.  Multi-GPU: rows py = row_first + k*row_step only
+// (cyclic row split); tiles index those rows densely.
+#include "ofl_internal.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileW = 8, kTileH = 4;  // one warp
+constexpr int kTilesPerUnit = 4;       // 32x4 pixels per queue pop
+
+struct MandelArgs {
+  uint32_t* out;
+  uint32_t width, height;
+  double re0, re1, im0, im1, esc;
+  uint32_t max_iter;
+  uint64_t limit;  // pixels gtid < limit are computed
+  uint32_t row_first, row_step, rows;  // rows owned by this launch
+  uint32_t tiles_x;
+  uint64_t units;
+};
+
+__device__ __forceinline__ uint32_t escape_count(double cre, double cim, double esc,
+                                                 uint32_t max_iter) {
+  double zr = 0.0, zi = 0.0;
+  uint32_t count = 0;
+  for (uint32_t i = 0; i < max_iter; ++i) {
+    const double zr2 = __dmul_rn(zr, zr);
+    const double zi2 = __dmul_rn(zi, zi);
+    if (__dadd_rn(zr2, zi2) > esc) break;
+    const double t = __dadd_rn(__dsub_rn(zr2, zi2), cre);
+    zi = __dadd_rn(__dmul_rn(__dmul_rn(2.0, zr), zi), cim);
+    zr = t;
+    ++count;
+  }
+  return count;
+}
+
+__global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned int* queue) {
+  const int lane = threadIdx.x & 31;
+  const double dre = __dsub_rn(a.re1, a.re0);
+  const double dim = __dsub_rn(a.im1, a.im0);
+  const double fw = (double)a.width, fh = (double)a.height;
+  const uint32_t tile_rows = (a.rows + kTileH - 1) / kTileH;
+  (void)tile_rows;
+  while (true) {
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(queue, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((uint64_t)u >= a.units) break;
+#pragma unroll 1
+    for (int k = 0; k < kTilesPerUnit; ++k) {
+      const uint64_t tile = (uint64_t)u * kTilesPerUnit + k;
+      const uint32_t ty = (uint32_t)(tile / a.tiles_x);
+      const uint32_t tx = (uint32_t)(tile % a.tiles_x);
+      const uint32_t px = tx * kTileW + (lane & (kTileW - 1));
+      const uint32_t r = ty * kTileH + (lane >> 3);  // dense row index
+      if (r >= a.rows || px >= a.width) continue;
+      const uint32_t py = a.row_first + r * a.row_step;
+      const uint64_t gtid = (uint64_t)py * a.width + px;
+      if (gtid >= a.limit) continue;
+      const double cre =
+          __dadd_rn(a.re0, __ddiv_rn(__dmul_rn(__dadd_rn((double)px, 0.5), dre), fw));
+      const double cim =
+          __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
+      a.out[gtid] = escape_count(cre, cim, a.esc, a.max_iter);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint32_t height,
+                              double re0, double re1, double im0, double im1, double esc,
+                              uint32_t max_iter, uint64_t items, uint32_t row_first,
+                              uint32_t row_step, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (row_step == 0) return ofl::set_error(OFL_ERR_BAD_ARGS, "row_step must be >= 1");
+  const uint64_t total = (uint64_t)((uint32_t)(width * height));  // u32 wrap as mandelbrot.k
+  const uint64_t limit = items < total ? items : total;
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  if (limit && width && row_first < height) {
+    MandelArgs a;
+    a.out = out;
+    a.width = width;
+    a.height = height;
+    a.re0 = re0;
+    a.re1 = re1;
+    a.im0 = im0;
+    a.im1 = im1;
+    a.esc = esc;
+    a.max_iter = max_iter;
+    a.limit = limit;
+    a.row_first = row_first;
+    a.row_step = row_step;
+    // rows of this launch that can hold a pixel with gtid < limit
+    const uint64_t last_row = (limit - 1) / width;  // highest py needed
+    const uint64_t max_py = last_row < (uint64_t)height - 1 ? last_row : (uint64_t)height - 1;
+    a.rows = max_py < row_first ? 0 : (uint32_t)((max_py - row_first) / row_step + 1);
+    a.tiles_x = (width + kTileW - 1) / kTileW;
+    const uint64_t tiles = (uint64_t)a.tiles_x * ((a.rows + kTileH - 1) / kTileH);
+    a.units = (tiles + kTilesPerUnit - 1) / kTilesPerUnit;
+    if (a.units) {
+      void* scratch = nullptr;
+      // queue word lives past the reductions' scratch (k_reduce.cu)
+      int st = ofl::stream_scratch(s, 65536, &scratch);
+      if (st) return st;
+      unsigned int* queue = reinterpret_cast<unsigned int*>(static_cast<char*>(scratch) + 32768);
+      cudaError_t e = cudaMemsetAsync(queue, 0, sizeof(unsigned int), s->cs);
+      if (e != cudaSuccess) return ofl::cuda_error(e, "queue reset");
+      uint64_t warps = a.units;
+      uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+      const uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 8;
+      if (blocks > cap) blocks = cap;
+      k_mandelbrot<<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      e = cudaPeekAtLastError();
+      if (e != cudaSuccess) return ofl::cuda_error(e, "mandelbrot launch");
+      ofl::count_launch();
+    }
+  }
+  return q.finish(ticket);
+}

@@ -1,0 +1,189 @@
+// 1-D 3-point stencil (stencil.k, /root/reference/pkg/src/offloadrt/bench/
+// kernels/stencil.k:2-10) and its iteration as a heat equation (BASELINE
+// config 2).
+//
+//   y[i] = x[i]                                   i == 0 or i == n-1
+//   y[i] = (0.5*x[i-1] + x[i]) + 0.5*x[i+1]       otherwise
+//
+// evaluated left to right with round-to-nearest and no contraction, exactly
+// the reference executor's order (kernel/codegen.py:241-289: every binary
+// operation is a separate IEEE operation).  Items are independent, so the
+// parallel order is free.
+//
+// Single step (k_stencil): each thread owns an aligned pair of cells loaded
+// as one 128-bit vector; the outer neighbours come from the adjacent lanes by
+// warp shuffle, so every cell is read from HBM once: 16 B/cell.
+//
+// Temporal blocking (k_heat_tb): a CTA stages a tile of kTile cells plus a
+// halo of `tb` cells each side in shared memory, advances it `tb` steps in
+// place (the valid region shrinks by one cell per side per step), and writes
+// the centre back: 16 B/cell per `tb` steps instead of per step.  Global
+// endpoints are fixed points of the update, exactly as stencil.k.
+#include "ofl_internal.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double point(double l, double c, double r) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(0.5, l), c), __dmul_rn(0.5, r));
+}
+
+// m  = number of items that execute (min(n, grid*block of the .k launch))
+// hi = highest readable x index = min(m, n-1)
+__global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__ x,
+                                                      double* __restrict__ y, uint64_t n,
+                                                      uint64_t m) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t hi = (m < n - 1) ? m : n - 1;
+  const uint64_t npairs = (m + 1) >> 1;
+  const uint64_t warp0 = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
+  for (uint64_t base = warp0 * 32; base < npairs; base += nwarps * 32) {
+    const uint64_t j = base + lane;
+    const uint64_t lo = 2 * j;
+    double2 v = make_double2(0.0, 0.0);
+    if (lo + 1 <= hi) {
+      v = __ldcs(reinterpret_cast<const double2*>(x) + j);
+    } else if (lo <= hi) {
+      v.x = x[lo];
+    }
+    double left = __shfl_up_sync(0xffffffffu, v.y, 1);
+    double right = __shfl_down_sync(0xffffffffu, v.x, 1);
+    if (lane == 0 && lo >= 1 && lo - 1 <= hi) left = x[lo - 1];
+    if (lane == 31 && lo + 2 <= hi) right = x[lo + 2];
+    if (lo < m) {
+      const double r0 = (lo == 0 || lo == n - 1) ? v.x : point(left, v.x, v.y);
+      if (lo + 1 < m) {
+        const double r1 = (lo + 1 == n - 1) ? v.y : point(v.x, v.y, right);
+        __stcs(reinterpret_cast<double2*>(y) + j, make_double2(r0, r1));
+      } else {
+        y[lo] = r0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- heat ---
+constexpr int kTbThreads = 512;
+constexpr int kTile = 8192;  // cells written per CTA pass
+
+// One pass = `tb` steps over the whole vector (x -> y).  Tile t covers
+// cells [t*kTile, (t+1)*kTile); smem holds [t*kTile - tb, (t+1)*kTile + tb).
+__global__ void __launch_bounds__(kTbThreads) k_heat_tb(const double* __restrict__ x,
+                                                        double* __restrict__ y, uint64_t n,
+                                                        int tb) {
+  extern __shared__ double sm[];  // two buffers of kTile + 2*tb
+  const int w = kTile + 2 * tb;
+  double* a = sm;
+  double* b = sm + w;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t g0 = (int64_t)(t * kTile) - tb;  // global index of smem[0]
+    for (int k = threadIdx.x; k < w; k += kTbThreads) {
+      const int64_t g = g0 + k;
+      a[k] = (g >= 0 && g < (int64_t)n) ? __ldcs(x + g) : 0.0;
+    }
+    __syncthreads();
+    for (int s = 1; s <= tb; ++s) {
+      // valid after s steps: smem [s, w - s)
+      for (int k = s + threadIdx.x; k < w - s; k += kTbThreads) {
+        const int64_t g = g0 + k;
+        double v;
+        if (g <= 0 || g >= (int64_t)n - 1) v = a[k];
+        else v = point(a[k - 1], a[k], a[k + 1]);
+        b[k] = v;
+      }
+      __syncthreads();
+      double* tmp = a;
+      a = b;
+      b = tmp;
+    }
+    for (int k = tb + threadIdx.x; k < tb + kTile; k += kTbThreads) {
+      const int64_t g = g0 + k;
+      if (g < (int64_t)n) __stcs(y + g, a[k]);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t items,
+                           uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  const uint64_t m = items < n ? items : n;
+  if (m && (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil operands must be 16-byte aligned");
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  if (m) {
+    const uint64_t npairs = (m + 1) >> 1;
+    uint64_t blocks = (npairs + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 8;
+    if (blocks > cap) blocks = cap;
+    k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(x, y, n, m);
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return ofl::cuda_error(e, "stencil launch");
+    ofl::count_launch();
+  }
+  return q.finish(ticket);
+}
+
+extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, int tb,
+                        uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (n < 1) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat needs n >= 1");
+  if (tb < 1 || tb > 64) return ofl::set_error(OFL_ERR_BAD_ARGS, "temporal block must be 1..64");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat operands must be 16-byte aligned");
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  const int sms = ofl::num_sms(s->dev);
+  double* src = x;
+  double* dst = y;
+  uint64_t left = steps;
+  const size_t smem = sizeof(double) * 2 * (kTile + 2 * 64);
+  // per-device attribute; cheap to (re)apply
+  cudaFuncSetAttribute(k_heat_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // Pass schedule: full passes of tb steps plus a remainder; the number of
+  // passes must have the parity of `steps` so the state ends where the
+  // single-step ping-pong would leave it (x if steps is even, else y).
+  uint64_t full = steps / (uint64_t)tb, rem = steps % (uint64_t)tb;
+  uint64_t passes = full + (rem ? 1 : 0);
+  bool split = (passes & 1) != (steps & 1);  // split one pass into (k-1, 1)
+  uint64_t launches = 0;
+  auto run_pass = [&](int k) -> cudaError_t {
+    if (k == 1) {
+      uint64_t npairs = (n + 1) >> 1;
+      uint64_t blocks = (npairs + kThreads - 1) / kThreads;
+      if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+      k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(src, dst, n, n);
+    } else {
+      const uint64_t ntiles = (n + kTile - 1) / kTile;
+      uint64_t blocks = ntiles < (uint64_t)sms * 2 ? ntiles : (uint64_t)sms * 2;
+      const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
+      k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
+    }
+    ++launches;
+    double* t = src;
+    src = dst;
+    dst = t;
+    return cudaPeekAtLastError();
+  };
+  while (left > 0) {
+    int k = (uint64_t)tb < left ? tb : (int)left;
+    cudaError_t e;
+    if (split && k >= 2) {
+      e = run_pass(k - 1);
+      if (e == cudaSuccess) e = run_pass(1);
+      split = false;
+    } else {
+      e = run_pass(k);
+    }
+    if (e != cudaSuccess) return ofl::cuda_error(e, "heat launch");
+    left -= (uint64_t)k;
+  }
+  ofl::count_launch(launches);
+  return q.finish(ticket);
+}

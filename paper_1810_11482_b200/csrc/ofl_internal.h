@@ -1,0 +1,79 @@
+// Internal declarations shared by the libofl.so translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "../../include/ofl.h"
+
+namespace ofl {
+
+// A completion marker: a CUDA event recorded right after ticket `ticket`.
+// Shared between the stream's marker list and any thread blocked on it; the
+// event returns to the per-device pool when the last holder lets go.
+struct EvBox {
+  int dev;
+  cudaEvent_t ev;
+  uint64_t ticket;
+  ~EvBox();
+};
+
+}  // namespace ofl
+
+struct ofl_stream {
+  int dev;
+  cudaStream_t cs;
+  std::mutex mu;                   // serialises enqueue + ticket assignment
+  uint64_t tail = 0;               // last ticket enqueued
+  std::atomic<uint64_t> done{0};   // highest ticket known complete
+  std::deque<std::shared_ptr<ofl::EvBox>> markers;  // ascending, placed lazily
+  // per-stream device scratch for multi-block reductions / work queues
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+struct ofl_event {
+  int dev;
+  cudaEvent_t ev;
+};
+
+namespace ofl {
+
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+cudaError_t use_device(int dev);
+int num_sms(int dev);
+void count_launch(uint64_t n = 1);
+// Scratch of at least `bytes` on the stream's device (caller holds s->mu).
+int stream_scratch(ofl_stream* s, size_t bytes, void** out);
+
+// RAII: locks the stream, makes its device current; finish() assigns the
+// ticket after the CUDA call(s) succeeded.
+struct Enqueue {
+  ofl_stream* s;
+  std::unique_lock<std::mutex> lk;
+  int status = OFL_OK;
+  explicit Enqueue(ofl_stream* st) : s(st), lk(st->mu) {
+    cudaError_t e = use_device(st->dev);
+    if (e != cudaSuccess) status = cuda_error(e, "cudaSetDevice");
+  }
+  bool ok() const { return status == OFL_OK; }
+  int finish(uint64_t* ticket) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "enqueue");
+    s->tail += 1;
+    if (ticket) *ticket = s->tail;
+    return OFL_OK;
+  }
+};
+
+}  // namespace ofl
+
+#define OFL_CHECK_STREAM(s) \
+  do { if (!(s)) return ofl::set_error(OFL_ERR_BAD_ARGS, "null stream"); } while (0)

@@ -1,0 +1,213 @@
+"""CUDA devices: discovery snapshot, streams, allocation.
+
+Replaces the reference DeviceObject (/root/reference/pkg/src/offloadrt/
+device.py:188-367), whose streams are FIFO queues drained by one OS thread
+each.  Here a stream id maps to a non-blocking CUDA stream owned by
+libofl.so; FIFO order per stream and overlap across streams come from the
+hardware, and no host thread sits between the caller and the device.
+
+Kept semantics: stream ids are plain ints, 0 is the default stream and
+``create_stream`` hands out 1, 2, ... (device.py:232-233); any id may be
+used and is materialised on first use; ``synchronize`` covers the streams
+that exist at call time (device.py:316-328).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import threading
+from collections import deque
+from dataclasses import dataclass
+from typing import Optional
+
+from . import _native
+from .completion import DeviceToken
+from .errors import BadArgsError
+from .futures import CompletionToken, make_ready, when_all
+
+DEFAULT_STREAM = 0
+
+
+@dataclass(frozen=True)
+class DeviceInfo:
+    """Discovery snapshot (reference device.py:37-48).  Capability compares
+    lexicographically on (major, minor)."""
+
+    name: str
+    capability: tuple
+    memory_bytes: int
+    compute_units: int
+
+    def meets(self, major: int, minor: int) -> bool:
+        return tuple(self.capability) >= (major, minor)
+
+
+@dataclass(frozen=True)
+class PhysicalInfo:
+    ordinal: int
+    product: str
+    capability: tuple
+    memory_bytes: int
+    sms: int
+    l2_bytes: int
+
+
+def query_physical(ordinal: int) -> PhysicalInfo:
+    lib = _native.load()
+    name = ctypes.create_string_buffer(256)
+    major, minor, sms = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    mem, l2 = ctypes.c_uint64(), ctypes.c_uint64()
+    _native.check(
+        lib.ofl_device_props(
+            ordinal, name, 256, ctypes.byref(major), ctypes.byref(minor), ctypes.byref(mem),
+            ctypes.byref(sms), ctypes.byref(l2),
+        ),
+        f"device {ordinal} properties",
+    )
+    return PhysicalInfo(
+        ordinal, name.value.decode(), (major.value, minor.value), mem.value, sms.value, l2.value
+    )
+
+
+class Stream:
+    """One CUDA stream plus host objects that must outlive its in-flight
+    operations (pinned sources, staging blocks)."""
+
+    __slots__ = ("ptr", "lib", "device", "sid", "_keep")
+
+    def __init__(self, device: "DeviceObject", sid: int):
+        self.lib = _native.load()
+        self.device = device
+        self.sid = sid
+        p = ctypes.c_void_p()
+        _native.check(self.lib.ofl_stream_create(device.ordinal, ctypes.byref(p)), "stream create")
+        self.ptr = p.value
+        self._keep: deque = deque()
+
+    def done_ticket(self) -> int:
+        return self.lib.ofl_stream_done(self.ptr)
+
+    def tail(self) -> int:
+        return self.lib.ofl_stream_tail(self.ptr)
+
+    def keep(self, ticket: int, release) -> None:
+        """Hold `release` (an object, or a callable run on release) until the
+        stream has completed `ticket`."""
+        self._keep.append((ticket, release))
+        self.purge()
+
+    def purge(self) -> None:
+        keep = self._keep
+        if not keep:
+            return
+        done = self.lib.ofl_stream_done(self.ptr)
+        if keep[0][0] > done and len(keep) > 32:
+            # long pipelines without observers: advance the watermark
+            ready = ctypes.c_int(0)
+            self.lib.ofl_query(self.ptr, keep[0][0], ctypes.byref(ready))
+            done = self.lib.ofl_stream_done(self.ptr)
+        while keep and keep[0][0] <= done:
+            try:
+                _, rel = keep.popleft()
+            except IndexError:
+                return
+            if callable(rel):
+                rel()
+
+    def token(self, ticket: int, finish=None) -> DeviceToken:
+        return DeviceToken(self, ticket, finish)
+
+    def tail_token(self) -> CompletionToken:
+        t = self.tail()
+        return DeviceToken(self, t) if t else make_ready(None)
+
+    def destroy(self) -> None:
+        if self.ptr:
+            self.lib.ofl_stream_destroy(self.ptr)
+            self.ptr = None
+            while self._keep:
+                _, rel = self._keep.popleft()
+                if callable(rel):
+                    rel()
+
+
+class DeviceObject:
+    """One logical device of a Runtime, bound to a physical CUDA ordinal."""
+
+    def __init__(self, info: DeviceInfo, physical: PhysicalInfo, record_events: bool = False):
+        self.info = info
+        self.physical = physical
+        self.ordinal = physical.ordinal
+        self.backend = "cuda"
+        self.record_events = record_events
+        self._lock = threading.Lock()
+        self._streams: dict[int, Stream] = {}
+        self._stream_ids = itertools.count(1)
+        self._allocated = 0
+        self._closed = False
+
+    # -- streams -------------------------------------------------------------
+    def create_stream(self) -> int:
+        return next(self._stream_ids)
+
+    def stream(self, sid: int) -> Stream:
+        s = self._streams.get(sid)
+        if s is not None:
+            return s
+        if not isinstance(sid, int) or isinstance(sid, bool) or sid < 0:
+            raise BadArgsError(f"invalid stream id {sid!r}")
+        with self._lock:
+            s = self._streams.get(sid)
+            if s is None:
+                if self._closed:
+                    raise BadArgsError(f"{self.info.name} is closed")
+                s = Stream(self, sid)
+                self._streams[sid] = s
+        return s
+
+    def synchronize(self) -> CompletionToken:
+        """Completes when everything enqueued so far on every existing stream
+        has completed (streams created later are not covered)."""
+        with self._lock:
+            streams = list(self._streams.values())
+        return when_all([s.tail_token() for s in streams])
+
+    # -- memory ----------------------------------------------------------------
+    def allocate(self, size: int) -> int:
+        lib = _native.load()
+        p = ctypes.c_void_p()
+        status = lib.ofl_malloc(self.ordinal, size, ctypes.byref(p))
+        if status:
+            raise _native.error_for(status, f"{self.info.name}: allocation of {size} bytes")
+        with self._lock:
+            self._allocated += size
+        return p.value
+
+    def release(self, ptr: int, size: int) -> None:
+        try:
+            _native.load().ofl_free(self.ordinal, ptr)
+        finally:
+            with self._lock:
+                self._allocated -= size
+
+    @property
+    def allocated_bytes(self) -> int:
+        return self._allocated
+
+    def close(self) -> None:
+        with self._lock:
+            streams = list(self._streams.values())
+            self._streams.clear()
+            self._closed = True
+        for s in streams:
+            s.destroy()
+
+
+def physical_devices() -> list[PhysicalInfo]:
+    n = _native.device_count()
+    return [query_physical(i) for i in range(n)]
+
+
+def describe(index: int, phys: PhysicalInfo, name: Optional[str] = None) -> DeviceInfo:
+    return DeviceInfo(name or f"cuda{index}", phys.capability, phys.memory_bytes, phys.sms)

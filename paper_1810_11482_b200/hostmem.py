@@ -1,0 +1,188 @@
+"""Pinned host memory: user-visible pinned arrays and the staging pool.
+
+The reference copies host data three times per write (handles.py:88,
+buffer.py:42,44-45 of /root/reference/pkg/src/offloadrt).  Here a write is:
+
+* zero-copy DMA when the source lies in pinned memory this runtime handed out
+  (``pinned_empty``) — the array is kept alive until the copy completes;
+* a direct ``cudaMemcpyAsync`` from pageable memory for small payloads (the
+  driver stages them before the call returns, so the caller may reuse them);
+* one host copy into a pinned staging block, then an async DMA, for large
+  pageable payloads (the block returns to the pool once the copy is done).
+
+Reads land in pinned memory (staging block or a pinned user array), because
+a device->pageable copy would block the calling thread.
+"""
+
+from __future__ import annotations
+
+import bisect
+import ctypes
+import threading
+import weakref
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+
+SMALL_PAGEABLE = 256 * 1024  # below this, let the driver stage pageable data
+_MIN_CLASS = 4096
+
+_ranges_lock = threading.Lock()
+_starts: list[int] = []
+_ends: list[int] = []
+
+
+def _register_range(start: int, size: int) -> None:
+    with _ranges_lock:
+        i = bisect.bisect_left(_starts, start)
+        _starts.insert(i, start)
+        _ends.insert(i, start + size)
+
+
+def _unregister_range(start: int) -> None:
+    with _ranges_lock:
+        i = bisect.bisect_left(_starts, start)
+        if i < len(_starts) and _starts[i] == start:
+            del _starts[i]
+            del _ends[i]
+
+
+def is_pinned(addr: int, size: int) -> bool:
+    """True if [addr, addr+size) lies inside one pinned allocation."""
+    if not _starts:
+        return False
+    i = bisect.bisect_right(_starts, addr) - 1
+    return i >= 0 and addr + size <= _ends[i]
+
+
+def _host_alloc(nbytes: int) -> int:
+    lib = _native.load()
+    p = ctypes.c_void_p()
+    _native.check(lib.ofl_host_alloc(max(1, nbytes), ctypes.byref(p)), "pinned allocation")
+    return p.value
+
+
+def _free(addr: int) -> None:
+    _unregister_range(addr)
+    try:
+        _native.load().ofl_host_free(addr)
+    except Exception:  # noqa: BLE001 - interpreter teardown
+        pass
+
+
+def _as_array(addr: int, nbytes: int) -> np.ndarray:
+    buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+    return np.frombuffer(buf, dtype=np.uint8)
+
+
+def pinned_empty(nbytes: int, dtype=np.uint8) -> np.ndarray:
+    """A numpy array in page-locked memory.  Writes from / reads into it are
+    zero-copy DMA.  Freed when the array (and every view of it) is gone."""
+    dtype = np.dtype(dtype)
+    count = nbytes // dtype.itemsize if dtype.itemsize else 0
+    size = max(1, count * dtype.itemsize)
+    addr = _host_alloc(size)
+    _register_range(addr, size)
+    owner = (ctypes.c_uint8 * size).from_address(addr)
+    # every numpy view keeps `owner` alive through its .base chain
+    weakref.finalize(owner, _free, addr)
+    raw = np.frombuffer(owner, dtype=np.uint8)
+    return raw[: count * dtype.itemsize].view(dtype)
+
+
+def pinned_like(src) -> np.ndarray:
+    """Pinned copy of an array-like (same dtype and shape)."""
+    a = np.ascontiguousarray(src)
+    out = pinned_empty(a.nbytes, a.dtype).reshape(a.shape)
+    np.copyto(out, a)
+    return out
+
+
+class Block:
+    """One reusable pinned staging block."""
+
+    __slots__ = ("addr", "size", "array")
+
+    def __init__(self, addr: int, size: int):
+        self.addr = addr
+        self.size = size
+        self.array = _as_array(addr, size)
+
+
+class StagingPool:
+    """Power-of-two size classes of pinned blocks, reused forever."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._free: dict[int, list[Block]] = {}
+
+    @staticmethod
+    def _cls(nbytes: int) -> int:
+        c = _MIN_CLASS
+        while c < nbytes:
+            c <<= 1
+        return c
+
+    def get(self, nbytes: int) -> Block:
+        c = self._cls(nbytes)
+        with self._lock:
+            lst = self._free.get(c)
+            if lst:
+                return lst.pop()
+        addr = _host_alloc(c)
+        return Block(addr, c)
+
+    def put(self, block: Block) -> None:
+        with self._lock:
+            self._free.setdefault(block.size, []).append(block)
+
+
+pool = StagingPool()
+
+
+def host_view(data) -> tuple[int, int, object]:
+    """(address, nbytes, owner) of a C-contiguous host buffer; owner keeps the
+    memory alive.  Non-buffer objects go through bytes() like the reference's
+    BufferHandle.enqueue_write (handles.py:88)."""
+    if isinstance(data, bytes):
+        n = len(data)
+        if n == 0:
+            return 0, 0, data
+        return ctypes.cast(ctypes.c_char_p(data), ctypes.c_void_p).value, n, data
+    if isinstance(data, np.ndarray) and data.flags.c_contiguous:
+        return data.ctypes.data, data.nbytes, data
+    try:
+        mv = memoryview(data)
+    except TypeError:
+        b = bytes(data)
+        return host_view(b)
+    if not mv.c_contiguous:
+        return host_view(mv.tobytes())
+    arr = np.frombuffer(mv.cast("B"), dtype=np.uint8) if mv.nbytes else np.zeros(0, np.uint8)
+    return (arr.ctypes.data if arr.size else 0), arr.nbytes, arr
+
+
+def writable_view(out) -> tuple[int, int, object]:
+    """(address, nbytes, owner) of a writable C-contiguous host buffer."""
+    if isinstance(out, np.ndarray):
+        if not out.flags.c_contiguous or not out.flags.writeable:
+            raise ValueError("output array must be C-contiguous and writable")
+        return out.ctypes.data, out.nbytes, out
+    mv = memoryview(out)
+    if mv.readonly or not mv.c_contiguous:
+        raise ValueError("output buffer must be C-contiguous and writable")
+    arr = np.frombuffer(mv.cast("B"), dtype=np.uint8)
+    return (arr.ctypes.data if arr.size else 0), arr.nbytes, arr
+
+
+def memcpy(dst: int, src: int, nbytes: int) -> None:
+    """Host copy (ctypes.memmove releases the GIL)."""
+    if nbytes:
+        ctypes.memmove(dst, src, nbytes)
+
+
+def free_block_later(stream, ticket: int, block: Optional[Block]) -> None:
+    if block is not None:
+        stream.keep(ticket, lambda: pool.put(block))

@@ -1,0 +1,186 @@
+"""Generate tests/golden/golden.json by running the REFERENCE implementation.
+
+Run in the build container (the reference is importable only here):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every expected output below comes from the reference package `offloadrt`
+executing the workload through its own public API on its `host` backend
+(numba whole-grid executor, /root/reference/pkg/src/offloadrt/kernel/
+codegen.py) — never from this repository's code.  STREAM and the T-step heat
+equation have no reference kernel; they are produced by the reference
+executor running the .k sources in paper_1810_11482_b200/kernels/ (same
+language), i.e. the reference's semantics applied to those programs.
+Inputs are regenerated from the recorded seeds (numpy default_rng).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+
+from offloadrt import Runtime  # noqa: E402  (reference package)
+from offloadrt.bench import kernel_source  # noqa: E402
+
+VIEWPORT = (-2.0, 1.0, -1.5, 1.5)
+
+
+def sha(b: bytes) -> str:
+    return hashlib.sha256(b).hexdigest()
+
+
+def mine(name: str) -> str:
+    with open(os.path.join(REPO, "paper_1810_11482_b200", "kernels", f"{name}.k")) as fh:
+        return fh.read()
+
+
+def run(device, source, kernel, args, items, block=256):
+    prog = device.create_program_with_source(source).get()
+    prog.build(kernel).get(timeout=600)
+    grid = (max(1, math.ceil(items / block)), 1, 1)
+    prog.run(args, kernel, grid, (block, 1, 1)).get(timeout=3600)
+
+
+def buf_with(device, data: bytes):
+    b = device.create_buffer(len(data)).get()
+    b.enqueue_write(0, data).get(timeout=600)
+    return b
+
+
+def main() -> None:
+    out: dict = {"generator": "tests/golden/make_golden.py", "reference": "offloadrt (host backend)"}
+    t0 = time.time()
+    with Runtime(backend="host") as rt:
+        dev = rt.get_all_devices().get()[0]
+
+        # -- stencil: hand case + random sizes (test_acceptance.py:62-66) ----
+        cases = []
+        x = np.array([1.0, 2.0, 3.0, 4.0])
+        xb, yb = buf_with(dev, x.tobytes()), dev.create_buffer(32).get()
+        run(dev, kernel_source("stencil"), "stencil", [xb, yb, 4], 4, 32)
+        cases.append({"n": 4, "input": x.tolist(),
+                      "output": np.frombuffer(yb.enqueue_read_sync(0, 32), np.float64).tolist()})
+        for n, seed in ((8, 101), (1024, 102), (1 << 20, 103)):
+            x = np.random.default_rng(seed).random(n)
+            xb, yb = buf_with(dev, x.tobytes()), dev.create_buffer(n * 8).get()
+            run(dev, kernel_source("stencil"), "stencil", [xb, yb, n], n, 32)
+            raw = yb.enqueue_read_sync(0, n * 8)
+            case = {"n": n, "seed": seed, "sha256": sha(raw)}
+            if n <= 1024:
+                case["output_hex"] = raw.hex()
+            cases.append(case)
+        out["stencil"] = cases
+
+        # -- heat: T applications, ping-pong (config 2 semantics) ------------
+        cases = []
+        for n, steps, seed in ((4096, 100, 201), (1 << 16, 10, 202)):
+            x = np.random.default_rng(seed).random(n)
+            a, b = buf_with(dev, x.tobytes()), dev.create_buffer(n * 8).get()
+            prog = dev.create_program_with_source(kernel_source("stencil")).get()
+            prog.build("stencil").get(timeout=600)
+            grid = (math.ceil(n / 256), 1, 1)
+            for s in range(steps):
+                src, dst = (a, b) if s % 2 == 0 else (b, a)
+                prog.run([src, dst, n], "stencil", grid, (256, 1, 1))
+            final = a if steps % 2 == 0 else b
+            raw = final.enqueue_read_sync(0, n * 8)
+            cases.append({"n": n, "steps": steps, "seed": seed, "sha256": sha(raw)})
+        out["heat"] = cases
+
+        # -- sum (test_bench.py:57-59, test_program.py:149-161, acceptance) --
+        cases = []
+        for values, label in ((np.array([2**32 - 1, 5], np.uint32), "wrap"),
+                              (np.ones(1000, np.uint32), "ones")):
+            ib, rb = buf_with(dev, values.tobytes()), dev.create_buffer(4).get()
+            run(dev, kernel_source("sum"), "sum", [ib, rb, len(values)], 32, 32)
+            cases.append({"label": label, "values": values.tolist(),
+                          "result": int(np.frombuffer(rb.enqueue_read_sync(0, 4), np.uint32)[0])})
+        for n, seed in ((8, 301), (1024, 302), (1 << 20, 303)):
+            values = np.random.default_rng(seed).integers(0, 2**32, size=n, dtype=np.uint32)
+            ib, rb = buf_with(dev, values.tobytes()), dev.create_buffer(4).get()
+            run(dev, kernel_source("sum"), "sum", [ib, rb, n], 32, 32)
+            cases.append({"n": n, "seed": seed,
+                          "result": int(np.frombuffer(rb.enqueue_read_sync(0, 4), np.uint32)[0])})
+        out["sum"] = cases
+
+        # -- mandelbrot (acceptance 16/64/256 @256; hand 3x3; origin) --------
+        cases = []
+        for w, h, max_iter, vp in (
+            (16, 16, 256, VIEWPORT), (64, 64, 256, VIEWPORT), (256, 256, 256, VIEWPORT),
+            (24, 16, 256, VIEWPORT), (3, 3, 64, (-0.5, 2.5, -1.5, 1.5)),
+            (3, 3, 50, (-1.5, 1.5, -1.5, 1.5)), (960, 540, 2000, VIEWPORT),
+        ):
+            ob = dev.create_buffer(w * h * 4).get()
+            run(dev, kernel_source("mandelbrot"), "mandelbrot",
+                [ob, w, h, *vp, 4.0, max_iter], w * h, 256)
+            raw = ob.enqueue_read_sync(0, w * h * 4)
+            counts = np.frombuffer(raw, np.uint32)
+            case = {"width": w, "height": h, "max_iter": max_iter, "viewport": list(vp),
+                    "esc": 4.0, "sha256": sha(raw), "sum": int(counts.astype(np.uint64).sum())}
+            if w * h <= 4096:
+                case["counts"] = counts.tolist()
+            cases.append(case)
+        if os.environ.get("GOLDEN_FULL_MANDELBROT", "1") == "1":
+            w, h, max_iter = 7680, 4320, 2000
+            ob = dev.create_buffer(w * h * 4).get()
+            t1 = time.time()
+            run(dev, kernel_source("mandelbrot"), "mandelbrot",
+                [ob, w, h, *VIEWPORT, 4.0, max_iter], w * h, 256)
+            raw = ob.enqueue_read_sync(0, w * h * 4)
+            counts = np.frombuffer(raw, np.uint32)
+            cases.append({"width": w, "height": h, "max_iter": max_iter,
+                          "viewport": list(VIEWPORT), "esc": 4.0, "sha256": sha(raw),
+                          "sum": int(counts.astype(np.uint64).sum()),
+                          "reference_seconds": round(time.time() - t1, 2)})
+        out["mandelbrot"] = cases
+
+        # -- partition (acceptance m=1 p=4; backend equivalence offset 17) ---
+        cases = []
+        for offset, count in ((17, 512), (9, 512), (0, 2_097_152), (4294967000, 1000)):
+            ob = dev.create_buffer(count * 8).get()
+            run(dev, kernel_source("partition"), "partition", [ob, offset, count], count, 256)
+            raw = ob.enqueue_read_sync(0, count * 8)
+            vals = np.frombuffer(raw, np.float64)
+            case = {"offset": offset, "count": count, "sha256": sha(raw),
+                    "max_abs_dev_from_1": float(np.abs(vals - 1.0).max())}
+            if count <= 1000:
+                case["output_hex"] = raw.hex()
+            cases.append(case)
+        out["partition"] = cases
+
+        # -- STREAM via the reference executor running kernels/stream.k ------
+        cases = []
+        n, s = 1 << 20, 3.0
+        rng = np.random.default_rng(401)
+        b = rng.random(n)
+        c = rng.random(n)
+        for op, args_of in (
+            ("copy", lambda A, B, C: [A, B, n]),
+            ("scale", lambda A, B, C: [A, B, s, n]),
+            ("add", lambda A, B, C: [A, B, C, n]),
+            ("triad", lambda A, B, C: [A, B, C, s, n]),
+        ):
+            A = dev.create_buffer(n * 8).get()
+            B, C = buf_with(dev, b.tobytes()), buf_with(dev, c.tobytes())
+            run(dev, mine("stream"), op, args_of(A, B, C), n, 256)
+            raw = A.enqueue_read_sync(0, n * 8)
+            cases.append({"op": op, "n": n, "seed": 401, "scalar": s, "sha256": sha(raw)})
+        out["stream"] = cases
+
+    out["seconds"] = round(time.time() - t0, 1)
+    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(f"wrote golden.json in {out['seconds']} s")
+
+
+if __name__ == "__main__":
+    sys.exit(main())
