@@ -165,6 +165,14 @@ int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double* res, uint
 int ofl_partition(ofl_stream* s, double* out, uint32_t offset, uint64_t count,
                   uint64_t* ticket);
 
+/* ---- raw-CUDA baseline for the futurization-overhead benchmark ----------
+ * `steps` x (cudaMemcpyAsync H2D of `bytes` from `src` + one small triad
+ * launch over n elements) on the stream, timed on the host clock.
+ * mode 0: stream order only; 1: event-chained steps; 2: sync every step. */
+int ofl_bench_raw_chain(ofl_stream* s, void* dst, const void* src, uint64_t bytes, double* a,
+                        const double* b, const double* c, uint64_t n, uint64_t steps, int mode,
+                        double* seconds);
+
 /* ---- NCCL (dlopen'ed; the process's already-loaded libnccl.so.2 wins) ---- */
 #define OFL_DT_U32 0
 #define OFL_DT_F64 1

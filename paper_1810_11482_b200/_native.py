@@ -91,6 +91,13 @@ _SIGNATURES = {
     "ofl_sum_u32": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_dot_f32": (c_int, [_c_stream, c_void_p, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_partition": (c_int, [_c_stream, c_void_p, c_uint32, c_uint64, _u64p]),
+    "ofl_bench_raw_chain": (
+        c_int,
+        [
+            _c_stream, c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p, c_uint64,
+            c_uint64, c_int, POINTER(c_double),
+        ],
+    ),
     "ofl_nccl_available": (c_int, [c_char_p]),
     "ofl_nccl_unique_id": (c_int, [c_char_p]),
     "ofl_nccl_init_all": (c_int, [c_int, POINTER(c_int), POINTER(c_void_p)]),

@@ -106,6 +106,9 @@ class DeviceToken(CompletionToken):
             return
         self._try_complete(value=value)
 
+    def _group_key(self):
+        return (self._stream, self._ticket)
+
     def _fail(self, status: int, what: str) -> None:
         with _lock:
             if self._claimed:

@@ -1,0 +1,50 @@
+// Raw-CUDA reference loops for the futurization-overhead benchmark
+// (BASELINE config 5): the same H2D copy + kernel launch chain
+// the futurized API issues, written directly against the CUDA runtime with
+// no tokens, no tickets and no Python.  (t_futurized - t_raw) / K is the
+// per-step overhead of the futures layer.
+#include <chrono>
+
+#include "ofl_internal.h"
+
+namespace {
+
+__global__ void k_triad_small(double* __restrict__ a, const double* __restrict__ b,
+                              const double* __restrict__ c, double s, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = __dadd_rn(b[i], __dmul_rn(s, c[i]));
+}
+
+}  // namespace
+
+// mode 0: stream order only, one sync at the end
+// mode 1: additionally record an event after each step and make the next step
+//         wait on it (cudaStreamWaitEvent) — explicit dependency chaining
+// mode 2: cudaStreamSynchronize after every step (round-trip latency)
+extern "C" int ofl_bench_raw_chain(ofl_stream* s, void* dst, const void* src, uint64_t bytes,
+                                   double* a, const double* b, const double* c, uint64_t n,
+                                   uint64_t steps, int mode, double* seconds) {
+  OFL_CHECK_STREAM(s);
+  std::lock_guard<std::mutex> g(s->mu);
+  cudaError_t e = ofl::use_device(s->dev);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "cudaSetDevice");
+  cudaEvent_t ev = nullptr;
+  if (mode == 1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  cudaStreamSynchronize(s->cs);
+  auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t k = 0; k < steps; ++k) {
+    if (mode == 1 && k) cudaStreamWaitEvent(s->cs, ev, 0);
+    cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s->cs);
+    k_triad_small<<<blocks ? blocks : 1, 256, 0, s->cs>>>(a, b, c, 3.0, n);
+    if (mode == 1) cudaEventRecord(ev, s->cs);
+    if (mode == 2) cudaStreamSynchronize(s->cs);
+  }
+  e = cudaStreamSynchronize(s->cs);
+  auto t1 = std::chrono::steady_clock::now();
+  if (ev) cudaEventDestroy(ev);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "raw chain");
+  *seconds = std::chrono::duration<double>(t1 - t0).count();
+  ofl::count_launch(steps);
+  return OFL_OK;
+}

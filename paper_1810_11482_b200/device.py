@@ -88,6 +88,15 @@ class Stream:
     def done_ticket(self) -> int:
         return self.lib.ofl_stream_done(self.ptr)
 
+    def wait_ticket(self, ticket: int) -> int:
+        """Block until `ticket` completed; returns the C status."""
+        return self.lib.ofl_wait(self.ptr, ticket)
+
+    def query_ticket(self, ticket: int) -> bool:
+        ready = ctypes.c_int(0)
+        status = self.lib.ofl_query(self.ptr, ticket, ctypes.byref(ready))
+        return bool(ready.value) and not status
+
     def tail(self) -> int:
         return self.lib.ofl_stream_tail(self.ptr)
 
