@@ -147,11 +147,12 @@ int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, in
 /* mandelbrot.k (bench/kernels/mandelbrot.k:6-29), pixels gtid in
  * [0, min(width*height mod 2^32, items)); counts written at out[gtid].
  * Rows py with (py - row_first) % row_step == 0 only (multi-GPU cyclic row
- * split; row_first=0,row_step=1 for the whole image). */
+ * split; row_first=0,row_step=1 for the whole image).  compact=1 packs the
+ * launch's rows densely: the k-th owned row lands at out[k*width ...]. */
 int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint32_t height,
                    double re0, double re1, double im0, double im1, double esc,
                    uint32_t max_iter, uint64_t items, uint32_t row_first,
-                   uint32_t row_step, uint64_t* ticket);
+                   uint32_t row_step, int compact, uint64_t* ticket);
 
 /* sum.k (bench/kernels/sum.k:3-11): res[0] = sum(in[0..n)) mod 2^32 */
 int ofl_sum_u32(ofl_stream* s, const uint32_t* in, uint32_t* res, uint64_t n,

@@ -85,7 +85,7 @@ _SIGNATURES = {
         c_int,
         [
             _c_stream, c_void_p, c_uint32, c_uint32, c_double, c_double, c_double, c_double,
-            c_double, c_uint32, c_uint64, c_uint32, c_uint32, _u64p,
+            c_double, c_uint32, c_uint64, c_uint32, c_uint32, c_int, _u64p,
         ],
     ),
     "ofl_sum_u32": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),

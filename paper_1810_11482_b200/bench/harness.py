@@ -1,0 +1,583 @@
+"""The reference's benchmark workloads on the CUDA runtime, plus the B200
+configurations of BASELINE.json.
+
+Mirrors /root/reference/pkg/src/offloadrt/bench/harness.py (configs,
+validators, run_stencil / run_partition / run_mandelbrot(_series) / run_sum,
+CSV rows) so callers of the reference harness switch over unchanged, and
+adds the multi-device compositions the reference never runs:
+
+* ``heat_multi``       — 1-D slab decomposition, halo exchange between
+                         devices every `halo` steps (config 2);
+* ``mandelbrot_multi`` — cyclic row split across devices, host-side image
+                         assembly overlapped with the remaining devices'
+                         compute (config 3);
+* ``dot_multi``        — partitioned fp32 dot product + one NCCL allreduce
+                         (config 4);
+* ``run_stream``       — STREAM copy/scale/add/triad (config 1).
+
+Every run validates its output before a time is reported, like the
+reference (harness.py:1-7); validators are vectorised numpy restatements of
+the kernels (the reference's own validator functions, harness.py:123-158).
+"""
+
+from __future__ import annotations
+
+import csv
+import math
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from ..bindings import kernel_source
+from ..errors import BadArgsError, ValidationFailedError
+from ..futures import task_pool, when_all
+from ..handles import BufferHandle, DeviceHandle, ProgramHandle, copy
+from ..hostmem import pinned_empty
+from .image import write_image
+from .timing import TimingProtocol, measure
+
+DEFAULT_SEED = 20180214
+VIEWPORT = (-2.0, 1.0, -1.5, 1.5)
+
+
+# -- configs (reference harness.py:45-95) -------------------------------------
+
+
+@dataclass(frozen=True)
+class StencilConfig:
+    n: int
+    block_x: int = 32
+
+    def __post_init__(self):
+        if self.n < 3:
+            raise BadArgsError("stencil needs n >= 3")
+
+
+@dataclass(frozen=True)
+class PartitionConfig:
+    m: int
+    partitions: int
+    block_size: int = 256
+
+    def __post_init__(self):
+        if not 1 <= self.m <= 8:
+            raise BadArgsError("partition m must be in 1..8")
+        if self.partitions < 1:
+            raise BadArgsError("partition count must be positive")
+
+    def vector_length(self, num_devices: int) -> int:
+        n = (2**self.m) * 1024 * self.block_size
+        return n * self.partitions if num_devices == 1 else n
+
+
+@dataclass(frozen=True)
+class MandelbrotConfig:
+    width: int
+    height: int
+    max_iter: int = 256
+    escape_radius: float = 2.0
+    viewport: tuple = VIEWPORT
+    async_write: bool = False
+
+    def __post_init__(self):
+        if self.width * self.height < 1:
+            raise BadArgsError("image must have at least one pixel")
+
+
+@dataclass(frozen=True)
+class BenchReport:
+    benchmark: str
+    backend: str
+    devices: int
+    partitions: int
+    n_or_pixels: int
+    mean_ms: float
+    validated: bool
+    config: dict = field(default_factory=dict, compare=False)
+
+
+CSV_FIELDS = ["benchmark", "backend", "devices", "partitions", "n_or_pixels", "mean_ms", "validated"]
+
+
+def append_csv(path, report: BenchReport) -> None:
+    fresh = not os.path.exists(path) or os.path.getsize(path) == 0
+    with open(path, "a", newline="") as fh:
+        w = csv.writer(fh)
+        if fresh:
+            w.writerow(CSV_FIELDS)
+        w.writerow([report.benchmark, report.backend, report.devices, report.partitions,
+                    report.n_or_pixels, f"{report.mean_ms:.6f}", "1" if report.validated else "0"])
+
+
+# -- validators (reference harness.py:123-158) ----------------------------------
+
+
+def stencil_oracle(x: np.ndarray) -> np.ndarray:
+    y = x.copy()
+    y[1:-1] = 0.5 * x[:-2] + x[1:-1] + 0.5 * x[2:]
+    return y
+
+
+def sum_oracle(values: np.ndarray) -> int:
+    return int(values.astype(np.uint64).sum()) & 0xFFFFFFFF
+
+
+def mandelbrot_oracle(cfg: MandelbrotConfig) -> np.ndarray:
+    w, h = cfg.width, cfg.height
+    re0, re1, im0, im1 = cfg.viewport
+    idx = np.arange(w * h, dtype=np.int64)
+    cre = re0 + ((idx % w).astype(np.float64) + 0.5) * (re1 - re0) / float(w)
+    cim = im0 + ((idx // w).astype(np.float64) + 0.5) * (im1 - im0) / float(h)
+    zr = np.zeros(idx.size)
+    zi = np.zeros(idx.size)
+    count = np.zeros(idx.size, dtype=np.uint32)
+    live = np.ones(idx.size, dtype=bool)
+    limit = cfg.escape_radius * cfg.escape_radius
+    for _ in range(cfg.max_iter):
+        live &= ~(zr * zr + zi * zi > limit)
+        if not live.any():
+            break
+        a, b = zr[live], zi[live]
+        t = a * a - b * b + cre[live]
+        zi[live] = 2.0 * a * b + cim[live]
+        zr[live] = t
+        count[live] += 1
+    return count
+
+
+def _expect_equal(actual: np.ndarray, expected: np.ndarray, what: str) -> None:
+    if actual.shape != expected.shape or not np.array_equal(actual, expected):
+        bad = np.flatnonzero(actual != expected) if actual.shape == expected.shape else [0]
+        i = int(bad[0]) if len(bad) else 0
+        raise ValidationFailedError(
+            f"{what}: first mismatch at index {i}: device={actual.flat[i]!r} "
+            f"oracle={expected.flat[i] if expected.size > i else None!r}"
+        )
+
+
+def _build(device: DeviceHandle, name: str, source: Optional[str] = None) -> ProgramHandle:
+    prog = device.create_program_with_source(source or kernel_source(name)).get()
+    prog.build(name).get()
+    return prog
+
+
+def _builtin(device: DeviceHandle, name: str) -> ProgramHandle:
+    prog = device.create_builtin_program().get()
+    prog.build(name).get()
+    return prog
+
+
+# -- stencil (reference harness.py:199-230) ---------------------------------------
+
+
+def run_stencil(cfg: StencilConfig, device: DeviceHandle,
+                protocol: TimingProtocol = TimingProtocol(), seed: int = DEFAULT_SEED) -> BenchReport:
+    x = np.random.default_rng(seed).random(cfg.n)
+    payload = x.tobytes()
+    xb = device.create_buffer(cfg.n * 8).get()
+    yb = device.create_buffer(cfg.n * 8).get()
+    prog = _build(device, "stencil")
+    grid, block = (math.ceil(cfg.n / cfg.block_x), 1, 1), (cfg.block_x, 1, 1)
+    result: dict = {}
+
+    def iteration():
+        xb.enqueue_write(0, payload)
+        prog.run([xb, yb, cfg.n], "stencil", grid, block)
+        result["out"] = yb.enqueue_read(0, cfg.n * 8).get()
+
+    mean_ms = measure(iteration, protocol)
+    _expect_equal(np.frombuffer(result["out"], np.float64), stencil_oracle(x), "stencil")
+    return BenchReport("stencil", "cuda", 1, 1, cfg.n, mean_ms, True,
+                       {"n": cfg.n, "block_x": cfg.block_x})
+
+
+# -- partition: the paper's Alg. 1 (reference harness.py:236-335) ---------------
+
+
+@dataclass
+class PartitionPart:
+    buffer: BufferHandle
+    program: ProgramHandle
+    stream: int
+    offset: int
+    count: int
+    payload: object
+    block_size: int
+
+
+def prepare_partitions(cfg: PartitionConfig, devices: Sequence[DeviceHandle],
+                       seed: int = DEFAULT_SEED, pinned: bool = True):
+    """One buffer + stream per partition, partition i on device i mod k; the
+    kernel is built once per device.  Payloads are staged in pinned memory
+    (zero-copy DMA) unless pinned=False."""
+    if not devices:
+        raise BadArgsError("partition needs at least one device")
+    n = cfg.vector_length(len(devices))
+    x = np.random.default_rng(seed).random(n)
+    programs = [_build(d, "partition") for d in devices]
+    base, extra = divmod(n, cfg.partitions)
+    parts, offset = [], 0
+    for i in range(cfg.partitions):
+        count = base + (1 if i < extra else 0)
+        dev = devices[i % len(devices)]
+        if pinned:
+            payload = pinned_empty(count * 8, np.float64)
+            payload[:] = x[offset : offset + count]
+        else:
+            payload = x[offset : offset + count].tobytes()
+        parts.append(PartitionPart(dev.create_buffer(count * 8).get(), programs[i % len(devices)],
+                                   dev.create_stream(), offset, count, payload, cfg.block_size))
+        offset += count
+    return n, parts
+
+
+def enqueue_partition_round(parts: Sequence[PartitionPart], into: Optional[list] = None) -> list:
+    """Alg. 1: three rounds of asynchronous enqueues — all writes, all runs,
+    all reads — ordered only by each partition's stream."""
+    for p in parts:
+        p.buffer.enqueue_write(0, p.payload, p.stream)
+    for p in parts:
+        p.program.run([p.buffer, p.offset, p.count], "partition",
+                      (math.ceil(p.count / p.block_size), 1, 1), (p.block_size, 1, 1), p.stream)
+    if into is not None:
+        return [p.buffer.enqueue_read_into(0, out, p.stream) for p, out in zip(parts, into)]
+    return [p.buffer.enqueue_read(0, p.count * 8, p.stream) for p in parts]
+
+
+def run_partition(cfg: PartitionConfig, devices: Sequence[DeviceHandle],
+                  protocol: TimingProtocol = TimingProtocol(), seed: int = DEFAULT_SEED,
+                  tolerance: float = 1e-12) -> BenchReport:
+    n, parts = prepare_partitions(cfg, devices, seed)
+    outs = [pinned_empty(p.count * 8, np.float64) for p in parts]
+
+    def iteration():
+        for t in enqueue_partition_round(parts, outs):
+            t.get()
+
+    mean_ms = measure(iteration, protocol)
+    out = np.concatenate(outs)
+    if out.size != n:
+        raise ValidationFailedError(f"partition returned {out.size} of {n} elements")
+    dev = np.abs(out - 1.0)
+    if dev.size and dev.max() > tolerance:
+        i = int(np.argmax(dev > tolerance))
+        raise ValidationFailedError(f"partition: element {i} is {out[i]!r}, expected 1.0 within {tolerance}")
+    return BenchReport("partition", "cuda", len(devices), cfg.partitions, n, mean_ms, True,
+                       {"m": cfg.m, "block_size": cfg.block_size})
+
+
+# -- mandelbrot (reference harness.py:341-437) --------------------------------------
+
+
+def compute_mandelbrot(cfg: MandelbrotConfig, device: DeviceHandle, protocol, validate=True):
+    pixels = cfg.width * cfg.height
+    out = device.create_buffer(pixels * 4).get()
+    prog = _build(device, "mandelbrot")
+    re0, re1, im0, im1 = cfg.viewport
+    esc = cfg.escape_radius * cfg.escape_radius
+    args = [out, cfg.width, cfg.height, re0, re1, im0, im1, esc, cfg.max_iter]
+    host = pinned_empty(pixels * 4, np.uint32)
+
+    def iteration():
+        prog.run(args, "mandelbrot", (math.ceil(pixels / 256), 1, 1), (256, 1, 1))
+        out.enqueue_read_into(0, host).get()
+
+    mean_ms = measure(iteration, protocol)
+    counts = np.array(host)
+    if validate:
+        _expect_equal(counts, mandelbrot_oracle(cfg), "mandelbrot")
+    return counts, mean_ms
+
+
+def run_mandelbrot(cfg: MandelbrotConfig, device: DeviceHandle,
+                   protocol: TimingProtocol = TimingProtocol(), image_path=None) -> BenchReport:
+    counts, mean_ms = compute_mandelbrot(cfg, device, protocol)
+    if image_path is not None:
+        write_image(counts, cfg.width, cfg.height, image_path, cfg.max_iter)
+    return BenchReport("mandelbrot", "cuda", 1, 1, cfg.width * cfg.height, mean_ms, True,
+                       {"width": cfg.width, "height": cfg.height, "max_iter": cfg.max_iter})
+
+
+@dataclass(frozen=True)
+class SeriesEvent:
+    kind: str
+    index: int
+    start: float
+    end: float
+
+
+def run_mandelbrot_series(sizes: Sequence[int], device: DeviceHandle,
+                          protocol: TimingProtocol = TimingProtocol(), async_write: bool = False,
+                          out_dir=None, write_fn: Optional[Callable] = None):
+    """Increasing square images; each is written to disk after it validates.
+    With async_write the write of image i runs on the task pool while image
+    i+1 computes (reference harness.py:393-437)."""
+    write_fn = write_fn or write_image
+    reports, events, writers = [], [], []
+
+    def emit(counts, cfg, index):
+        t0 = time.perf_counter()
+        if out_dir is not None:
+            path = os.path.join(out_dir, f"mandelbrot_{cfg.width}x{cfg.height}.ppm")
+            write_fn(counts, cfg.width, cfg.height, path, cfg.max_iter)
+        events.append(SeriesEvent("write", index, t0, time.perf_counter()))
+
+    for index, size in enumerate(sizes):
+        cfg = MandelbrotConfig(width=size, height=size, async_write=async_write)
+        t0 = time.perf_counter()
+        counts, mean_ms = compute_mandelbrot(cfg, device, protocol)
+        events.append(SeriesEvent("compute", index, t0, time.perf_counter()))
+        reports.append(BenchReport("mandelbrot", "cuda", 1, 1, size * size, mean_ms, True,
+                                   {"width": size, "height": size, "async_write": async_write}))
+        if async_write:
+            writers.append(task_pool().submit(emit, counts, cfg, index))
+        else:
+            emit(counts, cfg, index)
+    for w in writers:
+        w.result()
+    events.sort(key=lambda e: e.start)
+    return reports, events
+
+
+class MandelbrotTiles:
+    """Config 3 on several devices: rows r with r mod G == g go to device g
+    (cyclic split — contiguous bands leave devices idle); each
+    device packs its rows densely and reads them into a pinned host block;
+    the host scatters a device's rows into the image as soon as that
+    device's read completes, while the others are still computing."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
+                 viewport=VIEWPORT, esc: float = 4.0, stream: int = 0):
+        self.devices = list(devices)
+        self.width, self.height, self.max_iter = width, height, max_iter
+        self.viewport, self.esc, self.stream = viewport, esc, stream
+        G = len(self.devices)
+        self.rows = [len(range(g, height, G)) for g in range(G)]
+        self.bufs = [d.create_buffer(max(4, r * width * 4)).get() for d, r in zip(self.devices, self.rows)]
+        self.progs = [_builtin(d, "mandelbrot_rows") for d in self.devices]
+        self.hosts = [pinned_empty(max(1, r * width) * 4, np.uint32) for r in self.rows]
+
+    def enqueue(self) -> list:
+        G = len(self.devices)
+        re0, re1, im0, im1 = self.viewport
+        toks = []
+        for g in range(G):
+            if self.rows[g] == 0:
+                toks.append(None)
+                continue
+            self.progs[g].run([self.bufs[g], self.width, self.height, re0, re1, im0, im1, self.esc,
+                               self.max_iter, g, G], "mandelbrot_rows", (1, 1, 1), (1, 1, 1),
+                              self.stream)
+            toks.append(self.bufs[g].enqueue_read_into(0, self.hosts[g], self.stream))
+        return toks
+
+    def assemble(self, toks: list, image: np.ndarray) -> np.ndarray:
+        G = len(self.devices)
+        img = image.reshape(self.height, self.width)
+        for g, t in enumerate(toks):
+            if t is None:
+                continue
+            t.get()
+            img[g::G] = self.hosts[g][: self.rows[g] * self.width].reshape(-1, self.width)
+        return image
+
+    def __call__(self, image: Optional[np.ndarray] = None) -> np.ndarray:
+        image = image if image is not None else np.empty(self.width * self.height, np.uint32)
+        return self.assemble(self.enqueue(), image)
+
+
+def mandelbrot_multi(devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
+                     viewport=VIEWPORT, esc: float = 4.0) -> np.ndarray:
+    return MandelbrotTiles(devices, width, height, max_iter, viewport, esc)()
+
+
+# -- heat equation across devices (config 2) ---------------------------------------
+
+
+class HeatSlabs:
+    """1-D slab decomposition of the heat equation over several devices.
+
+    Device g owns cells [lo_g, hi_g) and keeps `halo` ghost cells on each
+    inner side.  Every `halo` steps it advances its slab with the temporal-
+    blocking heat builtin (the ghosts absorb the shrinking valid region),
+    then the owned boundary strips are copied into the neighbours' ghosts —
+    device-side copies ordered on the default streams of both ends, no host
+    round trip.  Global endpoints stay fixed because a slab's outer end is
+    either the true endpoint or a ghost that is overwritten before use."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], x: np.ndarray, halo: int = 1):
+        G = len(devices)
+        n = x.size
+        if halo < 1:
+            raise BadArgsError("halo must be >= 1")
+        self.devices = list(devices)
+        self.n, self.halo = n, halo
+        self.bounds = [n * g // G for g in range(G + 1)]
+        for g in range(G):
+            if self.bounds[g + 1] - self.bounds[g] < halo + 1:
+                raise BadArgsError("slabs must be longer than the halo")
+        self.left = [0 if g == 0 else halo for g in range(G)]
+        self.right = [0 if g == G - 1 else halo for g in range(G)]
+        self.length = [self.bounds[g + 1] - self.bounds[g] + self.left[g] + self.right[g]
+                       for g in range(G)]
+        self.a, self.b = [], []
+        for g, d in enumerate(self.devices):
+            lo = self.bounds[g] - self.left[g]
+            local = np.ascontiguousarray(x[lo : lo + self.length[g]])
+            A = d.create_buffer(self.length[g] * 8).get()
+            B = d.create_buffer(self.length[g] * 8).get()
+            A.enqueue_write(0, local.tobytes())
+            self.a.append(A)
+            self.b.append(B)
+        self.progs = [_builtin(d, "heat") for d in self.devices]
+
+    def _exchange(self, cur: list) -> list:
+        h = self.halo
+        toks = []
+        for g in range(len(self.devices) - 1):
+            Lg = self.length[g]
+            # my last h owned cells -> neighbour's left ghosts
+            toks.append(copy(cur[g], (Lg - self.right[g] - h) * 8, cur[g + 1], 0, h * 8))
+            # neighbour's first h owned cells -> my right ghosts
+            toks.append(copy(cur[g + 1], self.left[g + 1] * 8, cur[g], (Lg - self.right[g]) * 8, h * 8))
+        return toks
+
+    def run(self, steps: int):
+        cur, nxt = self.a, self.b
+        left = steps
+        toks = []
+        while left > 0:
+            k = min(self.halo, left)
+            for g, p in enumerate(self.progs):
+                L = self.length[g]
+                p.run([cur[g], nxt[g], L, k], "heat", (math.ceil(L / 256), 1, 1), (256, 1, 1))
+            if k % 2:
+                cur, nxt = nxt, cur
+            left -= k
+            if left > 0:
+                toks = self._exchange(cur)
+        self.a, self.b = cur, nxt
+        return when_all(toks) if toks else None
+
+    def gather(self) -> np.ndarray:
+        out = np.empty(self.n)
+        reads = []
+        for g in range(len(self.devices)):
+            owned = self.bounds[g + 1] - self.bounds[g]
+            reads.append((g, self.a[g].enqueue_read(self.left[g] * 8, owned * 8)))
+        for g, t in reads:
+            out[self.bounds[g] : self.bounds[g + 1]] = np.frombuffer(t.get(), np.float64)
+        return out
+
+
+def heat_multi(devices: Sequence[DeviceHandle], x: np.ndarray, steps: int, halo: int = 1) -> np.ndarray:
+    slabs = HeatSlabs(devices, np.asarray(x, dtype=np.float64), halo)
+    slabs.run(steps)
+    return slabs.gather()
+
+
+# -- sum (reference harness.py:443-477) --------------------------------------------
+
+
+def run_sum(n: int, device: DeviceHandle, protocol: TimingProtocol = TimingProtocol(),
+            seed: int = DEFAULT_SEED, values: Optional[np.ndarray] = None) -> BenchReport:
+    if n < 1:
+        raise BadArgsError("sum needs n >= 1")
+    if values is None:
+        values = np.random.default_rng(seed).integers(0, 2**32, size=n, dtype=np.uint32)
+    values = np.asarray(values, dtype=np.uint32)
+    payload = values.tobytes()
+    ib = device.create_buffer(n * 4).get()
+    rb = device.create_buffer(4).get()
+    prog = _build(device, "sum")
+    result: dict = {}
+
+    def iteration():
+        ib.enqueue_write(0, payload)
+        prog.run([ib, rb, n], "sum", (1, 1, 1), (32, 1, 1))
+        result["out"] = rb.enqueue_read(0, 4).get()
+
+    mean_ms = measure(iteration, protocol)
+    actual = int(np.frombuffer(result["out"], np.uint32)[0])
+    if actual != sum_oracle(values):
+        raise ValidationFailedError(f"sum: device={actual} oracle={sum_oracle(values)}")
+    return BenchReport("sum", "cuda", 1, 1, n, mean_ms, True, {"n": n})
+
+
+# -- STREAM (config 1) -----------------------------------------------------------------
+
+
+def run_stream(op: str, n: int, device: DeviceHandle, protocol: TimingProtocol = TimingProtocol(),
+               seed: int = DEFAULT_SEED, scalar: float = 3.0) -> BenchReport:
+    rng = np.random.default_rng(seed)
+    b, c = rng.random(n), rng.random(n)
+    A, B, C = (device.create_buffer(n * 8).get() for _ in range(3))
+    B.enqueue_write(0, b.tobytes())
+    C.enqueue_write(0, c.tobytes())
+    prog = _build(device, op, kernel_source("stream"))
+    args = {"copy": [A, B, n], "scale": [A, B, scalar, n], "add": [A, B, C, n],
+            "triad": [A, B, C, scalar, n]}[op]
+    grid, block = (math.ceil(n / 256), 1, 1), (256, 1, 1)
+
+    def iteration():
+        prog.run(args, op, grid, block).get()
+
+    mean_ms = measure(iteration, protocol)
+    got = np.frombuffer(A.enqueue_read(0, n * 8).get(), np.float64)
+    exp = {"copy": b, "scale": scalar * b, "add": b + c, "triad": b + scalar * c}[op]
+    _expect_equal(got, exp, f"stream {op}")
+    nbytes = (16 if op in ("copy", "scale") else 24) * n
+    return BenchReport(f"stream_{op}", "cuda", 1, 1, n, mean_ms, True,
+                       {"n": n, "gbs": nbytes / (mean_ms * 1e-3) / 1e9})
+
+
+# -- partitioned dot product + allreduce (config 4) ---------------------------------------
+
+
+class DotShards:
+    """a, b split contiguously over the devices; each device reduces its
+    shard to one fp64 partial (dot_f32 builtin) and an NCCL allreduce on the
+    same stream leaves the total on every device."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None):
+        G = len(devices)
+        n = a.size
+        self.devices = list(devices)
+        self.n = n
+        self.bounds = [n * g // G for g in range(G + 1)]
+        self.A, self.B, self.R = [], [], []
+        for g, d in enumerate(self.devices):
+            lo, hi = self.bounds[g], self.bounds[g + 1]
+            A = d.create_buffer(max(4, (hi - lo) * 4)).get()
+            B = d.create_buffer(max(4, (hi - lo) * 4)).get()
+            if hi > lo:
+                A.enqueue_write(0, np.ascontiguousarray(a[lo:hi]))
+                B.enqueue_write(0, np.ascontiguousarray(b[lo:hi]))
+            self.A.append(A)
+            self.B.append(B)
+            self.R.append(d.create_buffer(8).get())
+        self.progs = [_builtin(d, "dot_f32") for d in self.devices]
+        self.comm = comm
+
+    def enqueue(self):
+        for g, p in enumerate(self.progs):
+            m = self.bounds[g + 1] - self.bounds[g]
+            p.run([self.A[g], self.B[g], self.R[g], m], "dot_f32", (max(1, math.ceil(m / 256)), 1, 1),
+                  (256, 1, 1))
+        if self.comm is not None:
+            return self.comm.allreduce(self.R, count=1, dtype="f64")
+        return None
+
+    def result(self) -> float:
+        if self.comm is None:
+            return float(sum(np.frombuffer(r.enqueue_read(0, 8).get(), np.float64)[0] for r in self.R))
+        return float(np.frombuffer(self.R[0].enqueue_read(0, 8).get(), np.float64)[0])
+
+
+def dot_multi(devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None) -> float:
+    shards = DotShards(devices, a, b, comm)
+    shards.enqueue()
+    return shards.result()

@@ -139,7 +139,7 @@ def _mandel_launch(st, v, items, ticket):
     out, width, height, re0, re1, im0, im1, esc, max_iter = v
     return st.lib.ofl_mandelbrot(
         st.ptr, out.ptr, width, height, float(re0), float(re1), float(im0), float(im1),
-        float(esc), max_iter, items, 0, 1, ticket,
+        float(esc), max_iter, items, 0, 1, 0, ticket,
     )
 
 
@@ -216,6 +216,25 @@ def _heat_launch(st, v, items, ticket):
     return st.lib.ofl_heat(st.ptr, x.ptr, y.ptr, n, steps, heat_block(), ticket)
 
 
+def _rows_oob(v, items):
+    out, width, height = v[0], v[1], v[2]
+    row_first, row_step = v[9], v[10]
+    rows = 0 if row_first >= height or row_step == 0 else (height - row_first + row_step - 1) // row_step
+    need = rows * width
+    lo = out.elements("buffer_u32")
+    return lo if need > lo else None
+
+
+def _rows_launch(st, v, items, ticket):
+    out, width, height, re0, re1, im0, im1, esc, max_iter, row_first, row_step = v
+    if row_step == 0:
+        raise BadArgsError("mandelbrot_rows: row_step must be >= 1")
+    return st.lib.ofl_mandelbrot(
+        st.ptr, out.ptr, width, height, float(re0), float(re1), float(im0), float(im1),
+        float(esc), max_iter, (width * height) & M32, row_first, row_step, 1, ticket,
+    )
+
+
 BUILTIN_KERNELS = {
     # fp32 dot product with fp64 accumulation into out[0]
     "dot_f32": Binding(
@@ -226,11 +245,22 @@ BUILTIN_KERNELS = {
     "heat": Binding(
         "heat", ("buffer_f64", "buffer_f64", "scalar_u32", "scalar_u32"), _heat_launch, _heat_oob
     ),
+    # mandelbrot.k over rows row_first + k*row_step only, packed densely
+    # (multi-GPU cyclic row split; the launch shape is ignored)
+    "mandelbrot_rows": Binding(
+        "mandelbrot_rows",
+        ("buffer_u32", "scalar_u32", "scalar_u32", "scalar_f64", "scalar_f64", "scalar_f64",
+         "scalar_f64", "scalar_f64", "scalar_u32", "scalar_u32", "scalar_u32"),
+        _rows_launch,
+        _rows_oob,
+    ),
 }
 
 BUILTIN_PARAM_NAMES = {
     "dot_f32": ("a", "b", "out", "n"),
     "heat": ("x", "y", "n", "steps"),
+    "mandelbrot_rows": ("out", "width", "height", "re0", "re1", "im0", "im1", "esc",
+                        "max_iter", "row_first", "row_step"),
 }
 
 

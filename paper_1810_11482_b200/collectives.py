@@ -1,0 +1,110 @@
+"""NCCL collectives on runtime buffers (BASELINE config 4).
+
+The reference has no collective (cross-device traffic is
+read -> host -> write).  Here an allreduce is one ``ncclAllReduce`` enqueued
+on each participating buffer's default stream, in place, so a reduction
+kernel followed by the allreduce never touches the host; the returned
+token completes when every rank's stream has passed the collective.
+
+Two ways to form a communicator:
+
+* ``Communicator.single_process(rt, devices)`` — one process driving several
+  GPUs (ncclCommInitAll; the devices must be distinct physical GPUs, NCCL
+  refuses two ranks on one GPU);
+* ``Communicator.from_process_group(rt, device)`` — one process per GPU
+  under torchrun; the NCCL unique id travels over torch.distributed.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+from . import _native
+from .errors import BadArgsError
+from .futures import CompletionToken, when_all
+
+_DTYPES = {"u32": _native.DT_U32, "f64": _native.DT_F64, "f32": _native.DT_F32}
+_OPS = {"sum": _native.OP_SUM, "max": _native.OP_MAX}
+
+
+class Communicator:
+    def __init__(self, rt, devices: Sequence, comms: list):
+        self._rt = rt
+        self.devices = list(devices)
+        self._comms = comms
+
+    @classmethod
+    def single_process(cls, rt, devices: Sequence) -> "Communicator":
+        lib = _native.load()
+        _native.check(lib.ofl_nccl_available(_native.nccl_library_path().encode()), "nccl")
+        objs = [rt.local._device(d.gid) for d in devices]
+        ordinals = [o.ordinal for o in objs]
+        if len(set(ordinals)) != len(ordinals):
+            raise BadArgsError("NCCL needs one rank per physical GPU")
+        arr = (ctypes.c_int * len(ordinals))(*ordinals)
+        out = (ctypes.c_void_p * len(ordinals))()
+        _native.check(lib.ofl_nccl_init_all(len(ordinals), arr, out), "ncclCommInitAll")
+        return cls(rt, devices, [out[i] for i in range(len(ordinals))])
+
+    @classmethod
+    def from_process_group(cls, rt, device, group=None) -> "Communicator":
+        import torch.distributed as dist
+
+        lib = _native.load()
+        _native.check(lib.ofl_nccl_available(_native.nccl_library_path().encode()), "nccl")
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _native.check(lib.ofl_nccl_unique_id(uid), "ncclGetUniqueId")
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        comm = ctypes.c_void_p()
+        ordinal = rt.local._device(device.gid).ordinal
+        _native.check(
+            lib.ofl_nccl_init_rank(world, rank, ordinal, uid, ctypes.byref(comm)),
+            "ncclCommInitRank",
+        )
+        return cls(rt, [device], [comm.value])
+
+    def allreduce(self, buffers: Sequence, count: int, dtype: str = "f64", op: str = "sum",
+                  stream: int = 0) -> CompletionToken:
+        """In-place allreduce of the first `count` elements of each buffer
+        (one buffer per local rank, in device order)."""
+        if len(buffers) != len(self._comms):
+            raise BadArgsError("one buffer per local rank")
+        dt, ro = _DTYPES[dtype], _OPS[op]
+        lib = _native.load()
+        objs = [self._rt.local._buffer(b.gid) for b in buffers]
+        streams = [o.device.stream(stream) for o in objs]
+        if len(objs) == 1:
+            t = ctypes.c_uint64()
+            o, s = objs[0], streams[0]
+            _native.check(
+                lib.ofl_allreduce(self._comms[0], s.ptr, o.ptr, o.ptr, count, dt, ro,
+                                  ctypes.byref(t)),
+                "ncclAllReduce",
+            )
+            return s.token(t.value)
+        n = len(objs)
+        comms = (ctypes.c_void_p * n)(*self._comms)
+        sts = (ctypes.c_void_p * n)(*[s.ptr for s in streams])
+        ptrs = (ctypes.c_void_p * n)(*[o.ptr for o in objs])
+        tickets = (ctypes.c_uint64 * n)()
+        _native.check(
+            lib.ofl_allreduce_group(n, comms, sts, ptrs, ptrs, count, dt, ro, tickets),
+            "ncclAllReduce (group)",
+        )
+        return when_all([s.token(tickets[i]) for i, s in enumerate(streams)])
+
+    def close(self) -> None:
+        lib = _native.load()
+        for c in self._comms:
+            lib.ofl_comm_destroy(c)
+        self._comms = []
+
+
+def destroy(comm: Optional[Communicator]) -> None:
+    if comm is not None:
+        comm.close()

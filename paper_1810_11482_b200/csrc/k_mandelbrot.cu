@@ -32,6 +32,7 @@ struct MandelArgs {
   uint32_t row_first, row_step, rows;  // rows owned by this launch
   uint32_t tiles_x;
   uint64_t units;
+  int compact;  // 1: row r of this launch lands at out[r*width + px]
 };
 
 __device__ __forceinline__ uint32_t escape_count(double cre, double cim, double esc,
@@ -55,8 +56,6 @@ __global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned 
   const double dre = __dsub_rn(a.re1, a.re0);
   const double dim = __dsub_rn(a.im1, a.im0);
   const double fw = (double)a.width, fh = (double)a.height;
-  const uint32_t tile_rows = (a.rows + kTileH - 1) / kTileH;
-  (void)tile_rows;
   while (true) {
     unsigned int u = 0;
     if (lane == 0) u = atomicAdd(queue, 1u);
@@ -77,7 +76,8 @@ __global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned 
           __dadd_rn(a.re0, __ddiv_rn(__dmul_rn(__dadd_rn((double)px, 0.5), dre), fw));
       const double cim =
           __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
-      a.out[gtid] = escape_count(cre, cim, a.esc, a.max_iter);
+      const uint64_t at = a.compact ? (uint64_t)r * a.width + px : gtid;
+      a.out[at] = escape_count(cre, cim, a.esc, a.max_iter);
     }
   }
 }
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned 
 extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint32_t height,
                               double re0, double re1, double im0, double im1, double esc,
                               uint32_t max_iter, uint64_t items, uint32_t row_first,
-                              uint32_t row_step, uint64_t* ticket) {
+                              uint32_t row_step, int compact, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (row_step == 0) return ofl::set_error(OFL_ERR_BAD_ARGS, "row_step must be >= 1");
   const uint64_t total = (uint64_t)((uint32_t)(width * height));  // u32 wrap as mandelbrot.k
@@ -108,6 +108,7 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
     a.limit = limit;
     a.row_first = row_first;
     a.row_step = row_step;
+    a.compact = compact;
     // rows of this launch that can hold a pixel with gtid < limit
     const uint64_t last_row = (limit - 1) / width;  // highest py needed
     const uint64_t max_py = last_row < (uint64_t)height - 1 ? last_row : (uint64_t)height - 1;
