@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass
 from functools import lru_cache
 from typing import Callable, Optional
@@ -71,19 +72,15 @@ def _stream_binding(name: str, op: int, kinds: tuple) -> Binding:
         return a, b, c, s, n
 
     def oob(v, items):
-        a, b, c, _, n = unpack(v)
-        m = min(n, items)
-        lens = [a.elements("buffer_f64"), b.elements("buffer_f64")]
-        if c is not None:
-            lens.append(c.elements("buffer_f64"))
-        lo = min(lens)
+        m = v[-1] if v[-1] < items else items
+        lo = min(v[0].size_bytes, v[1].size_bytes, v[2].size_bytes if has_c else 1 << 62) >> 3
         return lo if m > lo else None
 
     def launch(st, v, items, ticket):
         a, b, c, s, n = unpack(v)
-        m = min(n, items)
         return st.lib.ofl_stream_op(
-            st.ptr, op, a.ptr, b.ptr, c.ptr if c is not None else b.ptr, float(s), m, ticket
+            st.ptr, op, a.ptr, b.ptr, c.ptr if c is not None else b.ptr, s,
+            n if n < items else items, ticket,
         )
 
     return Binding(name, kinds, launch, oob)
@@ -318,3 +315,15 @@ def check_oob(binding: Binding, values: list, items: int) -> Optional[OobAccessE
 
 def new_ticket():
     return ctypes.c_uint64()
+
+
+_tls = threading.local()
+
+
+def ticket_slot():
+    """Per-thread reusable c_uint64 the C side writes the ticket into."""
+    try:
+        return _tls.ticket
+    except AttributeError:
+        _tls.ticket = ctypes.c_uint64()
+        return _tls.ticket

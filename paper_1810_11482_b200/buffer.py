@@ -17,6 +17,7 @@ from .completion import DeviceToken
 from .device import DeviceObject
 from .errors import BadArgsError, OobAccessError
 from .futures import CompletionToken, make_ready
+from .bindings import ticket_slot as _ticket_slot
 
 ELEM_SIZE = {"buffer_f64": 8, "buffer_u32": 4, "buffer_f32": 4}
 
@@ -63,12 +64,14 @@ class BufferObject:
     # -- copies ------------------------------------------------------------------
     def enqueue_write(self, offset: int, data, stream: int = 0) -> CompletionToken:
         addr, n, owner = hostmem.host_view(data)
-        check_range(offset, n, self.size_bytes, "write")
-        st = self.device.stream(stream)
+        if offset < 0 or offset + n > self.size_bytes:
+            check_range(offset, n, self.size_bytes, "write")
+        dev = self.device
+        st = dev._streams.get(stream) or dev.stream(stream)
         lib = st.lib
-        ticket = ctypes.c_uint64()
+        ticket = _ticket_slot()
         dst = self.ptr + offset
-        if n == 0 or hostmem.is_pinned(addr, n):
+        if n == 0 or type(owner) is hostmem.PinnedArray or hostmem.is_pinned(addr, n):
             status = lib.ofl_h2d(st.ptr, dst, addr, n, ctypes.byref(ticket))
             if status:
                 raise_status(status, "write")

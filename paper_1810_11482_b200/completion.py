@@ -81,7 +81,11 @@ class DeviceToken(CompletionToken):
     __slots__ = ("_stream", "_ticket", "_finish", "_claimed")
 
     def __init__(self, stream, ticket: int, finish: Optional[Callable[[], Any]] = None):
-        super().__init__()
+        # CompletionToken.__init__ inlined: this runs once per device op
+        self._state = _PENDING
+        self._value = None
+        self._error = None
+        self._callbacks = None
         self._stream = stream
         self._ticket = ticket
         self._finish = finish

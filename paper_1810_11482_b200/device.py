@@ -92,6 +92,9 @@ class Stream:
         """Block until `ticket` completed; returns the C status."""
         return self.lib.ofl_wait(self.ptr, ticket)
 
+    def error(self, status: int) -> Exception:
+        return _native.error_for(status, f"{self.device.info.name} stream {self.sid}")
+
     def query_ticket(self, ticket: int) -> bool:
         ready = ctypes.c_int(0)
         status = self.lib.ofl_query(self.ptr, ticket, ctypes.byref(ready))
@@ -103,15 +106,17 @@ class Stream:
     def keep(self, ticket: int, release) -> None:
         """Hold `release` (an object, or a callable run on release) until the
         stream has completed `ticket`."""
-        self._keep.append((ticket, release))
-        self.purge()
+        keep = self._keep
+        keep.append((ticket, release))
+        if len(keep) & 15 == 0:
+            self.purge()
 
     def purge(self) -> None:
         keep = self._keep
         if not keep:
             return
         done = self.lib.ofl_stream_done(self.ptr)
-        if keep[0][0] > done and len(keep) > 32:
+        if keep[0][0] > done and len(keep) > 256:
             # long pipelines without observers: advance the watermark
             ready = ctypes.c_int(0)
             self.lib.ofl_query(self.ptr, keep[0][0], ctypes.byref(ready))

@@ -89,7 +89,35 @@ def pinned_empty(nbytes: int, dtype=np.uint8) -> np.ndarray:
     # every numpy view keeps `owner` alive through its .base chain
     weakref.finalize(owner, _free, addr)
     raw = np.frombuffer(owner, dtype=np.uint8)
-    return raw[: count * dtype.itemsize].view(dtype)
+    return raw[: count * dtype.itemsize].view(dtype).view(PinnedArray)
+
+
+class PinnedArray(np.ndarray):
+    """ndarray living in page-locked memory from ``pinned_empty``.  Its
+    address is looked up once per array object (numpy's own accessors cost
+    over a microsecond, which matters on the per-op path)."""
+
+    def __array_finalize__(self, obj):
+        self._ofl_addr = None
+
+    def _address(self) -> int:
+        addr = getattr(self, "_ofl_addr", None)
+        if addr is None:
+            addr = self.ctypes.data
+            self._ofl_addr = addr
+        return addr
+
+
+def _bytes_data_offset() -> int:
+    """Offset of a bytes object's payload from id(obj) (CPython layout),
+    verified against ctypes; 0 when the layout is not the expected one."""
+    probe = b"offset-probe"
+    off = bytes.__basicsize__ - 1
+    real = ctypes.cast(ctypes.c_char_p(probe), ctypes.c_void_p).value
+    return off if id(probe) + off == real else 0
+
+
+_BYTES_OFF = _bytes_data_offset()
 
 
 def pinned_like(src) -> np.ndarray:
@@ -146,11 +174,16 @@ def host_view(data) -> tuple[int, int, object]:
     """(address, nbytes, owner) of a C-contiguous host buffer; owner keeps the
     memory alive.  Non-buffer objects go through bytes() like the reference's
     BufferHandle.enqueue_write (handles.py:88)."""
-    if isinstance(data, bytes):
+    t = type(data)
+    if t is bytes:
         n = len(data)
         if n == 0:
             return 0, 0, data
+        if _BYTES_OFF:
+            return id(data) + _BYTES_OFF, n, data
         return ctypes.cast(ctypes.c_char_p(data), ctypes.c_void_p).value, n, data
+    if t is PinnedArray and data.flags.c_contiguous:
+        return data._address(), data.nbytes, data
     if isinstance(data, np.ndarray) and data.flags.c_contiguous:
         return data.ctypes.data, data.nbytes, data
     try:
@@ -166,6 +199,8 @@ def host_view(data) -> tuple[int, int, object]:
 
 def writable_view(out) -> tuple[int, int, object]:
     """(address, nbytes, owner) of a writable C-contiguous host buffer."""
+    if type(out) is PinnedArray and out.flags.c_contiguous and out.flags.writeable:
+        return out._address(), out.nbytes, out
     if isinstance(out, np.ndarray):
         if not out.flags.c_contiguous or not out.flags.writeable:
             raise ValueError("output array must be C-contiguous and writable")
