@@ -166,6 +166,20 @@ int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double* res, uint
 int ofl_partition(ofl_stream* s, double* out, uint32_t offset, uint64_t count,
                   uint64_t* ticket);
 
+/* ---- run-time compiled kernels: replace numba compile_ir
+ *      (kernel/codegen.py:319-337) for kernels with no hand-written binding.
+ *      NVRTC is dlopen'ed (toolkit copy first, `nvrtc_path` as a hint). ---- */
+typedef struct ofl_jit ofl_jit;
+int ofl_jit_available(const char* nvrtc_path);
+int ofl_jit_compile(int dev, const char* src, const char* entry, ofl_jit** out, char* log,
+                    int logcap);
+/* params: kernel parameter pointers (cudaLaunchKernel convention) */
+int ofl_jit_launch(ofl_stream* s, ofl_jit* k, void** params, uint64_t blocks, int threads,
+                   uint64_t* ticket);
+int ofl_jit_destroy(ofl_jit* k);
+/* 0xFF-fill device bytes in stream order (error-record reset) */
+int ofl_fill_ones(ofl_stream* s, void* dptr, uint64_t bytes, uint64_t* ticket);
+
 /* ---- raw-CUDA baseline for the futurization-overhead benchmark ----------
  * `steps` x (cudaMemcpyAsync H2D of `bytes` from `src` + one small triad
  * launch over n elements) on the stream, timed on the host clock.
@@ -173,6 +187,10 @@ int ofl_partition(ofl_stream* s, double* out, uint32_t offset, uint64_t count,
 int ofl_bench_raw_chain(ofl_stream* s, void* dst, const void* src, uint64_t bytes, double* a,
                         const double* b, const double* c, uint64_t n, uint64_t steps, int mode,
                         double* seconds);
+
+/* FP64 DMUL/DADD issue rate of the device (ops/s), the roofline denominator
+ * of the no-FMA Mandelbrot kernel. */
+int ofl_bench_fp64_peak(ofl_stream* s, double* ops_per_s);
 
 /* ---- NCCL (dlopen'ed; the process's already-loaded libnccl.so.2 wins) ---- */
 #define OFL_DT_U32 0

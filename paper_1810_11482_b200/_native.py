@@ -98,6 +98,12 @@ _SIGNATURES = {
             c_uint64, c_int, POINTER(c_double),
         ],
     ),
+    "ofl_bench_fp64_peak": (c_int, [_c_stream, POINTER(c_double)]),
+    "ofl_jit_available": (c_int, [c_char_p]),
+    "ofl_jit_compile": (c_int, [c_int, c_char_p, c_char_p, POINTER(c_void_p), c_char_p, c_int]),
+    "ofl_jit_launch": (c_int, [_c_stream, c_void_p, POINTER(c_void_p), c_uint64, c_int, _u64p]),
+    "ofl_jit_destroy": (c_int, [c_void_p]),
+    "ofl_fill_ones": (c_int, [_c_stream, c_void_p, c_uint64, _u64p]),
     "ofl_nccl_available": (c_int, [c_char_p]),
     "ofl_nccl_unique_id": (c_int, [c_char_p]),
     "ofl_nccl_init_all": (c_int, [c_int, POINTER(c_int), POINTER(c_void_p)]),

@@ -11,6 +11,8 @@
 // keeps kUnroll independent 128-bit loads per input in flight; loads bypass
 // L1 (.nc + L1::no_allocate), stores are evict-first (.cs) so the streamed
 // output does not displace anything useful from L2.
+#include <cstdlib>
+
 #include "ofl_internal.h"
 
 namespace {
@@ -43,34 +45,75 @@ __device__ __forceinline__ double2 apply2(double2 b, double2 c, double s) {
   return make_double2(apply<OP>(b.x, c.x, s), apply<OP>(b.y, c.y, s));
 }
 
-template <int OP>
-__global__ void __launch_bounds__(kThreads) k_stream_vec(double* __restrict__ a,
-                                                         const double* __restrict__ b,
-                                                         const double* __restrict__ c, double s,
-                                                         uint64_t n) {
+// Grid-stride form: a fixed grid of T-thread CTAs (MINB resident per SM)
+// sweeps the vector; each thread keeps U 128-bit loads per input in flight.
+template <int OP, int T, int U, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_stream_vec(double* __restrict__ a,
+                                                       const double* __restrict__ b,
+                                                       const double* __restrict__ c, double s,
+                                                       uint64_t n) {
   constexpr bool kC = (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD);
   const uint64_t n2 = n >> 1;
   double2* __restrict__ a2 = reinterpret_cast<double2*>(a);
   const double2* __restrict__ b2 = reinterpret_cast<const double2*>(b);
   const double2* __restrict__ c2 = reinterpret_cast<const double2*>(c);
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-  uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * T;
+  uint64_t i = (uint64_t)blockIdx.x * T + threadIdx.x;
 
-  for (; i + (kUnroll - 1) * stride < n2; i += kUnroll * stride) {
-    double2 vb[kUnroll], vc[kUnroll];
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 vb[U], vc[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       vb[u] = ld_stream(b2 + i + u * stride);
       if constexpr (kC) vc[u] = ld_stream(c2 + i + u * stride);
       else vc[u] = vb[u];
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) st_stream(a2 + i + u * stride, apply2<OP>(vb[u], vc[u], s));
+    for (int u = 0; u < U; ++u) st_stream(a2 + i + u * stride, apply2<OP>(vb[u], vc[u], s));
   }
   for (; i < n2; i += stride) {
     double2 vb = ld_stream(b2 + i);
     double2 vc = kC ? ld_stream(c2 + i) : vb;
     st_stream(a2 + i, apply2<OP>(vb, vc, s));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint64_t j = n - 1;
+    a[j] = apply<OP>(b[j], kC ? c[j] : 0.0, s);
+  }
+}
+
+// Tile form: one CTA per contiguous tile of T*U double2, no loop; the
+// hardware block scheduler load-balances the (many) tiles.
+template <int OP, int T, int U>
+__global__ void __launch_bounds__(T) k_stream_tile(double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  const double* __restrict__ c, double s,
+                                                  uint64_t n) {
+  constexpr bool kC = (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD);
+  const uint64_t n2 = n >> 1;
+  double2* __restrict__ a2 = reinterpret_cast<double2*>(a);
+  const double2* __restrict__ b2 = reinterpret_cast<const double2*>(b);
+  const double2* __restrict__ c2 = reinterpret_cast<const double2*>(c);
+  const uint64_t base = (uint64_t)blockIdx.x * (T * U) + threadIdx.x;
+  if (base + (U - 1) * T < n2) {
+    double2 vb[U], vc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vb[u] = ld_stream(b2 + base + u * T);
+      if constexpr (kC) vc[u] = ld_stream(c2 + base + u * T);
+      else vc[u] = vb[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_stream(a2 + base + u * T, apply2<OP>(vb[u], vc[u], s));
+  } else {
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = base + u * T;
+      if (i < n2) {
+        double2 vb = ld_stream(b2 + i);
+        double2 vc = kC ? ld_stream(c2 + i) : vb;
+        st_stream(a2 + i, apply2<OP>(vb, vc, s));
+      }
+    }
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const uint64_t j = n - 1;
@@ -89,21 +132,71 @@ __global__ void __launch_bounds__(kThreads) k_stream_scalar(double* a, const dou
     a[i] = apply<OP>(b[i], kC ? c[i] : 0.0, s);
 }
 
+template <int OP, int T, int U, int MINB>
+void launch_vec(cudaStream_t st, int sms, int per_sm, double* a, const double* b,
+                const double* c, double s, uint64_t n) {
+  uint64_t blocks = ((n >> 1) + (uint64_t)T * U - 1) / ((uint64_t)T * U);
+  const uint64_t cap = (uint64_t)sms * per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  k_stream_vec<OP, T, U, MINB><<<(unsigned)blocks, T, 0, st>>>(a, b, c, s, n);
+}
+
+template <int OP, int T, int U>
+void launch_tile(cudaStream_t st, double* a, const double* b, const double* c, double s,
+                 uint64_t n) {
+  uint64_t blocks = ((n >> 1) + (uint64_t)T * U - 1) / ((uint64_t)T * U);
+  if (blocks == 0) blocks = 1;
+  k_stream_tile<OP, T, U><<<(unsigned)blocks, T, 0, st>>>(a, b, c, s, n);
+}
+
+// Launch-shape variants (OFL_STREAM_VARIANT, for tuning sweeps); the default
+// is the one measured fastest on B200 (profiles/).
+int stream_variant() {
+  static int v = [] {
+    const char* e = getenv("OFL_STREAM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <int OP>
 cudaError_t launch(cudaStream_t st, int sms, double* a, const double* b, const double* c,
                    double s, uint64_t n) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
                          reinterpret_cast<uintptr_t>(c)) & 15) == 0;
-  // 8 resident 256-thread CTAs per SM (2048 threads); grid-stride beyond.
-  const uint64_t per_wave = (uint64_t)sms * 8;
-  const uint64_t units = aligned ? (n >> 1) : n;
-  uint64_t blocks = (units + kThreads * kUnroll - 1) / (kThreads * kUnroll);
-  if (blocks > per_wave) blocks = per_wave;
-  if (blocks == 0) blocks = 1;
-  if (aligned)
-    k_stream_vec<OP><<<(unsigned)blocks, kThreads, 0, st>>>(a, b, c, s, n);
-  else
-    k_stream_scalar<OP><<<(unsigned)blocks, kThreads, 0, st>>>(a, b, c, s, n);
+  if (!aligned) {
+    uint64_t blocks = (n + kThreads - 1) / kThreads;
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+    k_stream_scalar<OP><<<(unsigned)(blocks ? blocks : 1), kThreads, 0, st>>>(a, b, c, s, n);
+    return cudaPeekAtLastError();
+  }
+  switch (stream_variant()) {
+    case 1: launch_vec<OP, 256, 4, 4>(st, sms, 4, a, b, c, s, n); break;
+    case 2: launch_vec<OP, 256, 2, 8>(st, sms, 8, a, b, c, s, n); break;
+    case 3: launch_vec<OP, 512, 4, 2>(st, sms, 2, a, b, c, s, n); break;
+    case 4: launch_vec<OP, 128, 8, 8>(st, sms, 8, a, b, c, s, n); break;
+    case 5: launch_tile<OP, 256, 4>(st, a, b, c, s, n); break;
+    case 6: launch_tile<OP, 256, 2>(st, a, b, c, s, n); break;
+    case 7: launch_tile<OP, 128, 8>(st, a, b, c, s, n); break;
+    case 8: launch_vec<OP, 256, 8, 2>(st, sms, 4, a, b, c, s, n); break;
+    case 9: launch_vec<OP, kThreads, kUnroll, 1>(st, sms, 8, a, b, c, s, n); break;
+    case 10: launch_tile<OP, 256, 1>(st, a, b, c, s, n); break;
+    case 11: launch_tile<OP, 512, 1>(st, a, b, c, s, n); break;
+    case 12: launch_tile<OP, 512, 2>(st, a, b, c, s, n); break;
+    case 13: launch_tile<OP, 1024, 1>(st, a, b, c, s, n); break;
+    case 14: launch_tile<OP, 128, 4>(st, a, b, c, s, n); break;
+    case 15: launch_tile<OP, 128, 2>(st, a, b, c, s, n); break;
+    default:
+      // measured best on B200 (profiles/r01_stream_sweep.txt): one-shot tiles,
+      // 512 threads; 1 double2 per input per thread for the 2-input ops,
+      // 2 for the 1-input ops
+      if constexpr (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD)
+        launch_tile<OP, 512, 1>(st, a, b, c, s, n);
+      else
+        launch_tile<OP, 512, 2>(st, a, b, c, s, n);
+      break;
+  }
   return cudaPeekAtLastError();
 }
 

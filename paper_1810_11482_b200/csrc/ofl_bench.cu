@@ -17,6 +17,55 @@ __global__ void k_triad_small(double* __restrict__ a, const double* __restrict__
 
 }  // namespace
 
+// FP64 issue-rate probe for the Mandelbrot roofline: independent DMUL and
+// DADD chains (no FMA — the bit-exact kernel may not contract either).
+__global__ void k_fp64_peak(double* out, double a, double b, int iters) {
+  double x[8], y[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    x[k] = threadIdx.x + k;
+    y[k] = blockIdx.x + k;
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x[k] = __dmul_rn(x[k], a);
+      y[k] = __dadd_rn(y[k], b);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k] + y[k];
+  if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int ofl_bench_fp64_peak(ofl_stream* s, double* ops_per_s) {
+  OFL_CHECK_STREAM(s);
+  std::lock_guard<std::mutex> g(s->mu);
+  cudaError_t e = ofl::use_device(s->dev);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "cudaSetDevice");
+  double* out = nullptr;
+  cudaMalloc(&out, sizeof(double));
+  const int blocks = ofl::num_sms(s->dev) * 8, threads = 256, iters = 4096;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_fp64_peak<<<blocks, threads, 0, s->cs>>>(out, 0.999999, 1e-9, 64);  // warm-up
+  cudaEventRecord(a, s->cs);
+  k_fp64_peak<<<blocks, threads, 0, s->cs>>>(out, 0.999999, 1e-9, iters);
+  cudaEventRecord(b, s->cs);
+  e = cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "fp64 probe");
+  *ops_per_s = (double)blocks * threads * iters * 16 / (ms * 1e-3);
+  ofl::count_launch(2);
+  return OFL_OK;
+}
+
 // mode 0: stream order only, one sync at the end
 // mode 1: additionally record an event after each step and make the next step
 //         wait on it (cudaStreamWaitEvent) — explicit dependency chaining

@@ -137,15 +137,18 @@ class CudaDispatch:
     def build(self, program_gid: GlobalId, kernel_name: str) -> CompletionToken:
         return self._tokenized(lambda: self._program(program_gid).build(kernel_name))
 
-    def run(self, program_gid, kernel_name, grid, block, stream, args, device=None):
+    def run(self, program_gid, kernel_name, grid, block, stream, args, device=None, items=None):
+        """`items` may be passed by a caller that already validated the
+        launch shape (the handle does); otherwise it is derived here."""
         try:
             program = self._program(program_gid)
-            items = launch_items(grid, block)
+            if items is None:
+                items = launch_items(grid, block)
             resolved = [
                 ("buffer", self._buffer(value)) if tag == "buffer" else (tag, value)
                 for tag, value in args
             ]
-            return program.run(kernel_name, items, stream, resolved)
+            return program.run(kernel_name, items, stream, resolved, grid, block)
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 

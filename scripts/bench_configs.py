@@ -1,0 +1,293 @@
+#!/usr/bin/env python
+"""All BASELINE.json configurations on one B200, through the public API.
+
+    python scripts/bench_configs.py [--only stream,heat,mandel,dot,overhead,partition]
+                                    [--out profiles/rNN_configs.json]
+
+Device times are CUDA events on the launching stream (libofl.so events);
+every result is checked against the CPU oracle (oracle/) or the reference's
+golden vectors (tests/golden/golden.json) before it is reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import hashlib
+import json
+import math
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402  (checker only)
+from paper_1810_11482_b200 import Runtime, _native, make_ready, pinned_empty, when_all  # noqa: E402
+from paper_1810_11482_b200.bench.harness import (  # noqa: E402
+    PartitionConfig,
+    prepare_partitions,
+    enqueue_partition_round,
+)
+from paper_1810_11482_b200.bindings import kernel_source  # noqa: E402
+
+LIB = _native.load()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0}
+
+
+class Timer:
+    """CUDA events on one stream."""
+
+    def __init__(self, stream, ordinal=0):
+        self.stream = stream
+        self.a, self.b = ctypes.c_void_p(), ctypes.c_void_p()
+        LIB.ofl_event_create(ordinal, ctypes.byref(self.a))
+        LIB.ofl_event_create(ordinal, ctypes.byref(self.b))
+
+    def start(self):
+        LIB.ofl_event_record(self.a, self.stream.ptr)
+
+    def stop(self) -> float:
+        LIB.ofl_event_record(self.b, self.stream.ptr)
+        ms = ctypes.c_float()
+        _native.check(LIB.ofl_event_elapsed_ms(self.a, self.b, ctypes.byref(ms)), "elapsed")
+        return ms.value
+
+
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def stream_cfg(rt, dev, out):
+    st = rt.device_objects()[0].stream(0)
+    n = 1 << 25
+    rng = np.random.default_rng(1)
+    b, c = rng.random(n), rng.random(n)
+    A, B, C = (dev.create_buffer(n * 8).get() for _ in range(3))
+    B.enqueue_write(0, b)
+    C.enqueue_write(0, c)
+    prog = dev.create_program_with_source(kernel_source("stream")).get()
+    res = {}
+    for op, nbytes in (("copy", 16), ("scale", 16), ("add", 24), ("triad", 24)):
+        prog.build(op).get()
+        args = {"copy": [A, B, n], "scale": [A, B, 3.0, n], "add": [A, B, C, n],
+                "triad": [A, B, C, 3.0, n]}[op]
+        grid = ((n + 255) // 256, 1, 1)
+        for _ in range(10):
+            prog.run(args, op, grid, (256, 1, 1))
+        t = Timer(st)
+        K = 500
+        t.start()
+        for _ in range(K):
+            prog.run(args, op, grid, (256, 1, 1))
+        ms = t.stop() / K
+        got = np.frombuffer(A.enqueue_read(0, n * 8).get(), np.float64)
+        ok = got.tobytes() == oracle.stream(op, b, c, 3.0, threads=0).tobytes()
+        gbs = nbytes * n / (ms * 1e-3) / 1e9
+        res[op] = {"n": n, "us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
+                   "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
+                   "frac_8tbs_spec": round(gbs / 8000.0, 4), "bitexact": ok}
+    out["config1_stream"] = res
+
+
+def heat_cfg(rt, dev, out, steps=1000, n=1 << 28):
+    st = rt.device_objects()[0].stream(0)
+    res = {}
+    # parity at N=2^20, T=1000 against the oracle (bit-exact), per schedule
+    xs = np.random.default_rng(3).random(1 << 20)
+    expect = oracle.heat(xs, 1000, threads=0).tobytes()
+    prog = dev.create_builtin_program().get()
+    prog.build("heat").get()
+    X = dev.create_buffer(n * 8).get()
+    Y = dev.create_buffer(n * 8).get()
+    x = np.random.default_rng(20180214).random(n)
+    finals = {}
+    for tb in (1, 4, 8, 16, 32):
+        os.environ["OFL_HEAT_TB"] = str(tb)
+        Xs = dev.create_buffer(xs.nbytes).get()
+        Ys = dev.create_buffer(xs.nbytes).get()
+        Xs.enqueue_write(0, xs)
+        prog.run([Xs, Ys, xs.size, 1000], "heat", (xs.size // 256, 1, 1), (256, 1, 1))
+        small_ok = Xs.enqueue_read(0, xs.nbytes).get() == expect
+        X.enqueue_write(0, x)
+        dev.synchronize().get()
+        t = Timer(st)
+        t.start()
+        prog.run([X, Y, n, steps], "heat", (n // 256, 1, 1), (256, 1, 1))
+        ms = t.stop()
+        final = X if steps % 2 == 0 else Y
+        digest = sha(final.enqueue_read(0, 1 << 20).get())  # leading 1 MiB fingerprint
+        finals[tb] = digest
+        alg = 16.0 * n * steps
+        res[f"tb{tb}"] = {"ms_total": round(ms, 2), "us_per_step": round(ms * 1e3 / steps, 2),
+                          "effective_gbs": round(alg / (ms * 1e-3) / 1e9, 1),
+                          "frac_measured_hbm_effective": round(alg / (ms * 1e-3) / 1e9 / peaks()["hbm_gbs"], 4),
+                          "parity_2^20_T1000_bitexact": small_ok}
+    res["schedules_agree_bitexact"] = len(set(finals.values())) == 1
+    res["n"], res["steps"] = n, steps
+    res["note"] = ("effective GB/s counts the algorithmic 16 B/cell/step; with temporal "
+                   "blocking (tb>1) the HBM traffic is ~16 B/cell per tb steps, so this "
+                   "can exceed the HBM roofline")
+    os.environ.pop("OFL_HEAT_TB", None)
+    out["config2_heat"] = res
+
+
+def mandel_cfg(rt, dev, out, golden):
+    st = rt.device_objects()[0].stream(0)
+    w, h, it = 7680, 4320, 2000
+    O = dev.create_buffer(w * h * 4).get()
+    prog = dev.create_program_with_source(kernel_source("mandelbrot")).get()
+    prog.build("mandelbrot").get()
+    args = [O, w, h, -2.0, 1.0, -1.5, 1.5, 4.0, it]
+    grid = ((w * h + 255) // 256, 1, 1)
+    for _ in range(3):
+        prog.run(args, "mandelbrot", grid, (256, 1, 1))
+    t = Timer(st)
+    K = 20
+    t.start()
+    for _ in range(K):
+        prog.run(args, "mandelbrot", grid, (256, 1, 1))
+    ms = t.stop() / K
+    host = pinned_empty(w * h * 4, np.uint32)
+    O.enqueue_read_into(0, host).get()
+    ok = sha(host) == golden["mandelbrot"][7]["sha256"]
+    total_iters = int(host.astype(np.uint64).sum())
+    # FP64 ops per counted iteration: 4 mul + 4 add/sub; + 3 for the final test
+    escaped = int((host < it).sum())
+    dp_ops = 8 * total_iters + 3 * escaped
+    fp64 = fp64_peak(rt)
+    e2e_host = pinned_empty(w * h * 4, np.uint32)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        prog.run(args, "mandelbrot", grid, (256, 1, 1))
+        O.enqueue_read_into(0, e2e_host).get()
+    e2e_ms = (time.perf_counter() - t0) / 5 * 1e3
+    out["config3_mandelbrot"] = {
+        "width": w, "height": h, "max_iter": it, "kernel_ms": round(ms, 3),
+        "e2e_ms_with_d2h": round(e2e_ms, 3), "sha256_matches_reference": ok,
+        "total_iterations": total_iters, "dp_ops": dp_ops,
+        "achieved_dp_tops": round(dp_ops / (ms * 1e-3) / 1e12, 3),
+        "fp64_peak_measured_tops": fp64, "frac_fp64": round(dp_ops / (ms * 1e-3) / 1e12 / fp64, 4)
+        if fp64 else None,
+    }
+
+
+def fp64_peak(rt) -> float:
+    fn = getattr(LIB, "ofl_bench_fp64_peak", None)
+    if fn is None:
+        return None
+    fn.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double)]
+    fn.restype = ctypes.c_int
+    st = rt.device_objects()[0].stream(0)
+    v = ctypes.c_double()
+    if fn(st.ptr, ctypes.byref(v)):
+        return None
+    return round(v.value / 1e12, 3)
+
+
+def dot_cfg(rt, dev, out, n=1 << 31):
+    st = rt.device_objects()[0].stream(0)
+    A = dev.create_buffer(n * 4).get()
+    B = dev.create_buffer(n * 4).get()
+    R = dev.create_buffer(8).get()
+    rng = np.random.default_rng(20180214)
+    chunk = 1 << 27
+    a_all = np.empty(n, np.float32)
+    b_all = np.empty(n, np.float32)
+    for lo in range(0, n, chunk):
+        a_all[lo : lo + chunk] = rng.random(min(chunk, n - lo), dtype=np.float32)
+        b_all[lo : lo + chunk] = rng.random(min(chunk, n - lo), dtype=np.float32)
+    for lo in range(0, n, chunk):
+        A.enqueue_write(lo * 4, a_all[lo : lo + chunk])
+        B.enqueue_write(lo * 4, b_all[lo : lo + chunk])
+    prog = dev.create_builtin_program().get()
+    prog.build("dot_f32").get()
+    grid = (n // 256, 1, 1)
+    for _ in range(3):
+        prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
+    t = Timer(st)
+    K = 20
+    t.start()
+    for _ in range(K):
+        prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
+    ms = t.stop() / K
+    got = float(np.frombuffer(R.enqueue_read(0, 8).get(), np.float64)[0])
+    exp = oracle.dot_f32(a_all, b_all, threads=0)
+    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+    out["config4_dot"] = {"n": n, "kernel_ms": round(ms, 3), "gbs": round(gbs, 1),
+                          "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
+                          "result": got, "oracle": exp, "rel_err": abs(got - exp) / abs(exp),
+                          "within_1e-5": abs(got - exp) <= 1e-5 * abs(exp)}
+
+
+def overhead_cfg(rt, dev, out):
+    from bench import overhead_sweep  # noqa: E402
+
+    sweep = {}
+    for k in (1, 10, 100, 1000, 10000, 100000):
+        r = overhead_sweep(dev, rt, k, min(k, 2000))
+        sweep[str(k)] = r
+    out["config5_overhead"] = sweep
+
+
+def partition_cfg(rt, dev, out):
+    res = {}
+    for m in (1, 2, 3, 6):
+        cfg = PartitionConfig(m=m, partitions=4)
+        n, parts = prepare_partitions(cfg, [dev])
+        outs = [pinned_empty(p.count * 8, np.float64) for p in parts]
+        for _ in range(2):
+            for t in enqueue_partition_round(parts, outs):
+                t.get()
+        samples = []
+        for _ in range(11):
+            t0 = time.perf_counter()
+            for t in enqueue_partition_round(parts, outs):
+                t.get()
+            samples.append(time.perf_counter() - t0)
+        mean_ms = sum(samples[1:]) / 10 * 1e3
+        dev_max = float(max(np.abs(o - 1.0).max() for o in outs))
+        res[f"m{m}"] = {"n": n, "mean_ms": round(mean_ms, 3), "max_abs_dev": dev_max,
+                        "h2d_d2h_gbs": round(16.0 * n / (mean_ms * 1e-3) / 1e9, 2)}
+    out["alg1_partition"] = res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="stream,heat,mandel,dot,overhead,partition")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    with open(os.path.join(REPO, "tests", "golden", "golden.json")) as fh:
+        golden = json.load(fh)
+    out = {"device": None}
+    with Runtime(devices=[0]) as rt:
+        dev = rt.get_all_devices().get()[0]
+        out["device"] = rt.device_objects()[0].physical.product
+        for name in args.only.split(","):
+            t0 = time.time()
+            {"stream": lambda: stream_cfg(rt, dev, out),
+             "heat": lambda: heat_cfg(rt, dev, out),
+             "mandel": lambda: mandel_cfg(rt, dev, out, golden),
+             "dot": lambda: dot_cfg(rt, dev, out),
+             "overhead": lambda: overhead_cfg(rt, dev, out),
+             "partition": lambda: partition_cfg(rt, dev, out)}[name]()
+            print(f"[{name}] {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
+    text = json.dumps(out, indent=1)
+    print(text)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(text)
+
+
+if __name__ == "__main__":
+    main()

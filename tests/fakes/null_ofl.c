@@ -62,3 +62,9 @@ int ofl_nccl_init_rank(int n, int r, int d, const char* id, void** c) { (void)n;
 int ofl_allreduce(void* c, void* s, const void* a, void* b, uint64_t n, int d, int o, uint64_t* t) { (void)c; (void)s; (void)a; (void)b; (void)n; (void)d; (void)o; (void)t; return 8; }
 int ofl_allreduce_group(int n, void** c, void** s, void** a, void** b, uint64_t k, int d, int o, uint64_t* t) { (void)n; (void)c; (void)s; (void)a; (void)b; (void)k; (void)d; (void)o; (void)t; return 8; }
 int ofl_comm_destroy(void* c) { (void)c; return 0; }
+int ofl_bench_fp64_peak(void* s, double* v) { (void)s; *v = 0; return 0; }
+int ofl_jit_available(const char* p) { (void)p; return 3; }
+int ofl_jit_compile(int d, const char* s, const char* e, void** o, char* l, int c) { (void)d; (void)s; (void)e; (void)o; (void)l; (void)c; return 3; }
+int ofl_jit_launch(void* s, void* k, void** p, uint64_t b, int t, uint64_t* tk) { (void)k; (void)p; (void)b; (void)t; return op(s, tk); }
+int ofl_jit_destroy(void* k) { (void)k; return 0; }
+int ofl_fill_ones(void* s, void* d, uint64_t n, uint64_t* t) { memset(d, 0xff, n); return op(s, t); }

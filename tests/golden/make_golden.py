@@ -56,6 +56,95 @@ def buf_with(device, data: bytes):
     return b
 
 
+SEMANTICS_SRC = """
+kernel semantics(a : buffer_f64, b : buffer_u32, s : scalar_f64, m : scalar_u32) {
+    if (gtid < u32(8)) {
+        let fi = f64(gtid);
+        let x = s * fi + 0.125;
+        let wrapped = (m + gtid) * 4294967295;
+        let q = (m + 10) / (gtid + 1);
+        let picked = select(x > 1.0 && gtid != 3, sqrt(abs(x)), min(x, 2.0));
+        let trig = sin(x) * cos(x);
+        let clipped = max(u32(x * 100.0), wrapped);
+        let acc = 0.0;
+        for i in 0 .. 6 {
+            acc = acc + f64(i) * 0.5;
+            break if (acc > 4.0);
+        }
+        a[gtid] = picked + trig + acc + f64(q);
+        b[gtid] = clipped;
+    }
+}
+"""
+
+# (source, kernel, buffers [(kind, n)], scalars, grid, block)
+LANG_CASES = [
+    (SEMANTICS_SRC, "semantics", [("f64", 8), ("u32", 8)], [1.75, 123456789], (1, 1, 1), (8, 1, 1)),
+    (SEMANTICS_SRC, "semantics", [("f64", 8), ("u32", 8)], [-2.5, 4294967295], (2, 1, 1), (4, 1, 1)),
+    ("kernel w(out : buffer_u32, a : scalar_u32, b : scalar_u32) { out[0] = a * b; out[1] = a - b; }",
+     "w", [("u32", 2)], [4000000000, 4000000001], (1, 1, 1), (1, 1, 1)),
+    ("kernel d(out : buffer_u32, a : scalar_u32, b : scalar_u32) { out[0] = a / b; }",
+     "d", [("u32", 1)], [7, 2], (1, 1, 1), (1, 1, 1)),
+    ("kernel d(out : buffer_f64, b : scalar_f64) { out[0] = 1.0 / b; }",
+     "d", [("f64", 1)], [0.0], (1, 1, 1), (1, 1, 1)),
+    ("kernel o(out : buffer_f64, i : scalar_u32) { out[i] = 1.0; }",
+     "o", [("f64", 4)], [9], (1, 1, 1), (1, 1, 1)),
+    ("kernel n(out : buffer_f64) { out[gtid - 1] = 1.0; }", "n", [("f64", 4)], [], (1, 1, 1), (1, 1, 1)),
+    ("""kernel b(blocks : buffer_u32, threads : buffer_u32, dims : buffer_u32) {
+    blocks[gtid] = block_idx;
+    threads[gtid] = thread_idx;
+    if (gtid == 0) { dims[0] = grid_dim; dims[1] = block_dim; }
+}""", "b", [("u32", 12), ("u32", 12), ("u32", 2)], [], (3, 1, 1), (2, 2, 1)),
+    ("""kernel s(out : buffer_f64, flag : scalar_u32) {
+    if (gtid == 0) { let hit = 0.0; if (flag == 1 && out[99] > 0.0) { hit = 1.0; } out[0] = hit; }
+}""", "s", [("f64", 4)], [0], (1, 1, 1), (1, 1, 1)),
+    ("""kernel s(out : buffer_f64, flag : scalar_u32) {
+    if (gtid == 0) { let hit = 0.0; if (flag == 1 && out[99] > 0.0) { hit = 1.0; } out[0] = hit; }
+}""", "s", [("f64", 4)], [1], (1, 1, 1), (1, 1, 1)),
+    ("""kernel s(out : buffer_f64, flag : scalar_u32) {
+    if (gtid == 0) { if (flag == 1) { let t = 2.5; out[0] = t; } else { let t = 7; out[0] = f64(t); } }
+}""", "s", [("f64", 1)], [0], (1, 1, 1), (1, 1, 1)),
+    ("""kernel l(out : buffer_u32, n : scalar_u32) {
+    if (gtid == 0) { let total = 0; for i in 0 .. n { let double = i * 2; total = total + double; } out[0] = total; }
+}""", "l", [("u32", 1)], [5], (1, 1, 1), (1, 1, 1)),
+    ("kernel c(out : buffer_u32, x : scalar_f64) { out[gtid] = u32(x); }",
+     "c", [("u32", 1)], [-3.7], (1, 1, 1), (1, 1, 1)),
+    ("kernel c(out : buffer_u32, x : scalar_f64) { out[gtid] = u32(x); }",
+     "c", [("u32", 1)], [1e19], (1, 1, 1), (1, 1, 1)),
+    ("""kernel poly(y : buffer_f64, x : buffer_f64, n : scalar_u32) {
+    if (gtid < n) { let v = x[gtid]; y[gtid] = ((v * 3.0 - 1.5) * v + 0.25) / (v + 2.0); }
+}""", "poly", [("f64", 1000), ("f64", 1000)], [1000], (4, 1, 1), (256, 1, 1)),
+]
+
+
+def lang_cases(dev) -> list:
+    from offloadrt.errors import OffloadError
+
+    res = []
+    for src, name, bufs, scalars, grid, block in LANG_CASES:
+        prog = dev.create_program_with_source(src).get()
+        prog.build(name).get(timeout=600)
+        handles, inits = [], []
+        rng = np.random.default_rng(len(res))
+        for kind, n in bufs:
+            dt = np.float64 if kind == "f64" else np.uint32
+            init = (rng.random(n) if kind == "f64" else np.zeros(n)).astype(dt)
+            h = dev.create_buffer(n * dt().itemsize).get()
+            h.enqueue_write(0, init.tobytes()).get()
+            handles.append(h)
+            inits.append(init.tobytes().hex())
+        err = None
+        try:
+            prog.run(handles + scalars, name, grid, block).get(timeout=600)
+        except OffloadError as exc:
+            err = [type(exc).__name__, str(exc)]
+        outs = [h.enqueue_read_sync(0, h.size_bytes).hex() for h in handles]
+        res.append({"source": src, "kernel": name, "buffers": bufs, "scalars": scalars,
+                    "grid": list(grid), "block": list(block), "inputs_hex": inits,
+                    "outputs_hex": outs, "error": err})
+    return res
+
+
 def main() -> None:
     out: dict = {"generator": "tests/golden/make_golden.py", "reference": "offloadrt (host backend)"}
     t0 = time.time()
@@ -175,6 +264,9 @@ def main() -> None:
             raw = A.enqueue_read_sync(0, n * 8)
             cases.append({"op": op, "n": n, "seed": 401, "scalar": s, "sha256": sha(raw)})
         out["stream"] = cases
+
+        # -- generic kernel-language semantics (NVRTC path) -----------------
+        out["lang"] = lang_cases(dev)
 
     out["seconds"] = round(time.time() - t0, 1)
     with open(os.path.join(HERE, "golden.json"), "w") as fh:

@@ -273,12 +273,17 @@ def test_kernel_oob_fails_token_with_index(dev):
         s.run([i, r, 11], "sum", (1, 1, 1), (1, 1, 1)).get(timeout=5)
 
 
-def test_unbound_kernel_is_a_compile_error(dev):
-    p = dev.create_program_with_source(
-        "kernel w(out : buffer_u32, a : scalar_u32) { out[0] = a * a; }"
-    ).get()
+def test_unbound_kernel_goes_through_nvrtc(dev, monkeypatch):
+    src = "kernel w(out : buffer_u32, a : scalar_u32) { out[0] = a * a; }"
+    p = dev.create_program_with_source(src).get()
+    p.build("w").get(timeout=120)
+    out = dev.create_buffer(4).get()
+    p.run([out, 4_000_000_000], "w", (1, 1, 1), (1, 1, 1)).get()
+    assert np.frombuffer(out.enqueue_read_sync(0, 4), np.uint32)[0] == (4_000_000_000**2) % 2**32
+    monkeypatch.setenv("OFL_NO_JIT", "1")
+    q = dev.create_program_with_source(src).get()
     with pytest.raises(CompileError, match="sm_100a"):
-        p.build("w").get()
+        q.build("w").get()
 
 
 def test_renamed_kernel_still_binds(dev):
