@@ -36,6 +36,7 @@ from ..errors import BadArgsError, ValidationFailedError
 from ..futures import task_pool, when_all
 from ..handles import BufferHandle, DeviceHandle, ProgramHandle, copy
 from ..hostmem import pinned_empty
+from . import decomp
 from .image import write_image
 from .timing import TimingProtocol, measure
 
@@ -355,7 +356,7 @@ class MandelbrotTiles:
         self.width, self.height, self.max_iter = width, height, max_iter
         self.viewport, self.esc, self.stream = viewport, esc, stream
         G = len(self.devices)
-        self.rows = [len(range(g, height, G)) for g in range(G)]
+        self.rows = [len(decomp.cyclic_rows(height, G, g)) for g in range(G)]
         self.bufs = [d.create_buffer(max(4, r * width * 4)).get() for d, r in zip(self.devices, self.rows)]
         self.progs = [_builtin(d, "mandelbrot_rows") for d in self.devices]
         self.hosts = [pinned_empty(max(1, r * width) * 4, np.uint32) for r in self.rows]
@@ -415,17 +416,17 @@ class HeatSlabs:
             raise BadArgsError("halo must be >= 1")
         self.devices = list(devices)
         self.n, self.halo = n, halo
-        self.bounds = [n * g // G for g in range(G + 1)]
-        for g in range(G):
-            if self.bounds[g + 1] - self.bounds[g] < halo + 1:
-                raise BadArgsError("slabs must be longer than the halo")
-        self.left = [0 if g == 0 else halo for g in range(G)]
-        self.right = [0 if g == G - 1 else halo for g in range(G)]
-        self.length = [self.bounds[g + 1] - self.bounds[g] + self.left[g] + self.right[g]
-                       for g in range(G)]
+        try:
+            self.layout = decomp.slabs(n, G, halo)
+        except ValueError as exc:
+            raise BadArgsError(str(exc)) from None
+        self.bounds = decomp.shard_bounds(n, G)
+        self.left = [s.left for s in self.layout]
+        self.right = [s.right for s in self.layout]
+        self.length = [s.length for s in self.layout]
         self.a, self.b = [], []
         for g, d in enumerate(self.devices):
-            lo = self.bounds[g] - self.left[g]
+            lo = self.layout[g].start
             local = np.ascontiguousarray(x[lo : lo + self.length[g]])
             A = d.create_buffer(self.length[g] * 8).get()
             B = d.create_buffer(self.length[g] * 8).get()
@@ -435,15 +436,8 @@ class HeatSlabs:
         self.progs = [_builtin(d, "heat") for d in self.devices]
 
     def _exchange(self, cur: list) -> list:
-        h = self.halo
-        toks = []
-        for g in range(len(self.devices) - 1):
-            Lg = self.length[g]
-            # my last h owned cells -> neighbour's left ghosts
-            toks.append(copy(cur[g], (Lg - self.right[g] - h) * 8, cur[g + 1], 0, h * 8))
-            # neighbour's first h owned cells -> my right ghosts
-            toks.append(copy(cur[g + 1], self.left[g + 1] * 8, cur[g], (Lg - self.right[g]) * 8, h * 8))
-        return toks
+        return [copy(cur[sg], s_cell * 8, cur[dg], d_cell * 8, cells * 8)
+                for sg, s_cell, dg, d_cell, cells in decomp.halo_exchanges(self.layout, self.halo)]
 
     def run(self, steps: int):
         cur, nxt = self.a, self.b
@@ -547,7 +541,7 @@ class DotShards:
         n = a.size
         self.devices = list(devices)
         self.n = n
-        self.bounds = [n * g // G for g in range(G + 1)]
+        self.bounds = decomp.shard_bounds(n, G)
         self.A, self.B, self.R = [], [], []
         for g, d in enumerate(self.devices):
             lo, hi = self.bounds[g], self.bounds[g + 1]
