@@ -15,6 +15,9 @@
 // kTilesPerUnit tiles from an atomic queue so the slow (bounded) regions do
 // not leave SMs idle.  Multi-GPU: rows py = row_first + k*row_step only
 // (cyclic row split); tiles index those rows densely.
+#include <cmath>
+#include <cstdlib>
+
 #include "ofl_internal.h"
 
 namespace {
@@ -35,14 +38,23 @@ struct MandelArgs {
   int compact;  // 1: row r of this launch lands at out[r*width + px]
 };
 
+// INTCMP: the escape test `mag > esc` done on the bit patterns (int64
+// compare on the ALU pipe instead of DSETP on the FP64 pipe).  Exact when
+// mag >= +0 and esc > 0 are finite, which the host guarantees by enabling it
+// only for esc in (0, 1e10] and a viewport inside [-1e10, 1e10]: then every
+// executed iteration starts from |z|^2 <= 1e10 and nothing overflows.
+template <bool INTCMP>
 __device__ __forceinline__ uint32_t escape_count(double cre, double cim, double esc,
                                                  uint32_t max_iter) {
   double zr = 0.0, zi = 0.0;
   uint32_t count = 0;
+  const long long esc_bits = __double_as_longlong(esc);
+#pragma unroll 4
   for (uint32_t i = 0; i < max_iter; ++i) {
     const double zr2 = __dmul_rn(zr, zr);
     const double zi2 = __dmul_rn(zi, zi);
-    if (__dadd_rn(zr2, zi2) > esc) break;
+    const double mag = __dadd_rn(zr2, zi2);
+    if (INTCMP ? (__double_as_longlong(mag) > esc_bits) : (mag > esc)) break;
     const double t = __dadd_rn(__dsub_rn(zr2, zi2), cre);
     zi = __dadd_rn(__dmul_rn(__dmul_rn(2.0, zr), zi), cim);
     zr = t;
@@ -51,6 +63,7 @@ __device__ __forceinline__ uint32_t escape_count(double cre, double cim, double 
   return count;
 }
 
+template <bool INTCMP>
 __global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned int* queue) {
   const int lane = threadIdx.x & 31;
   const double dre = __dsub_rn(a.re1, a.re0);
@@ -77,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned 
       const double cim =
           __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
       const uint64_t at = a.compact ? (uint64_t)r * a.width + px : gtid;
-      a.out[at] = escape_count(cre, cim, a.esc, a.max_iter);
+      a.out[at] = escape_count<INTCMP>(cre, cim, a.esc, a.max_iter);
     }
   }
 }
@@ -128,7 +141,13 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
       const uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 8;
       if (blocks > cap) blocks = cap;
-      k_mandelbrot<<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      const double lim = 1e10;
+      const bool intcmp = esc > 0.0 && esc <= lim && fabs(re0) <= lim && fabs(re1) <= lim &&
+                          fabs(im0) <= lim && fabs(im1) <= lim && getenv("OFL_MANDEL_FPCMP") == nullptr;
+      if (intcmp)
+        k_mandelbrot<true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      else
+        k_mandelbrot<false><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       e = cudaPeekAtLastError();
       if (e != cudaSuccess) return ofl::cuda_error(e, "mandelbrot launch");
       ofl::count_launch();

@@ -19,6 +19,8 @@
 // place (the valid region shrinks by one cell per side per step), and writes
 // the centre back: 16 B/cell per `tb` steps instead of per step.  Global
 // endpoints are fixed points of the update, exactly as stencil.k.
+#include <cstdlib>
+
 #include "ofl_internal.h"
 
 namespace {
@@ -31,16 +33,15 @@ __device__ __forceinline__ double point(double l, double c, double r) {
 
 // m  = number of items that execute (min(n, grid*block of the .k launch))
 // hi = highest readable x index = min(m, n-1)
+// One-shot tiles (as the STREAM kernels: the block scheduler balances many
+// small CTAs better than a persistent grid): thread j owns cells 2j, 2j+1.
 __global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__ x,
                                                       double* __restrict__ y, uint64_t n,
                                                       uint64_t m) {
   const int lane = threadIdx.x & 31;
   const uint64_t hi = (m < n - 1) ? m : n - 1;
-  const uint64_t npairs = (m + 1) >> 1;
-  const uint64_t warp0 = ((uint64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * kThreads) >> 5;
-  for (uint64_t base = warp0 * 32; base < npairs; base += nwarps * 32) {
-    const uint64_t j = base + lane;
+  {
+    const uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
     const uint64_t lo = 2 * j;
     double2 v = make_double2(0.0, 0.0);
     if (lo + 1 <= hi) {
@@ -107,6 +108,78 @@ __global__ void __launch_bounds__(kTbThreads) k_heat_tb(const double* __restrict
   }
 }
 
+// Register-blocked temporal blocking.  A CTA of kRegThreads threads holds a
+// tile of kRegThreads*R consecutive cells in registers (thread t owns cells
+// [t*R, t*R+R) of the tile), advances it `tb` steps without touching memory
+// — in-warp neighbours by shuffle, warp-edge cells through a double-
+// buffered shared array, one __syncthreads per step — and writes the centre
+// kRegThreads*R - 2*tb cells.  Errors from the clamped tile ends travel one
+// cell per step, so they stay inside the tb-cell halo.  Shared-memory
+// traffic per cell-step drops from ~32 B (k_heat_tb) to ~2 warp-edge words,
+// which leaves the FP64 pipe (4 DP ops per cell-step) as the limiter.
+constexpr int kRegThreads = 256;
+
+template <int R>
+__global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restrict__ x,
+                                                          double* __restrict__ y, uint64_t n,
+                                                          int tb) {
+  constexpr int kWarps = kRegThreads / 32;
+  constexpr int kCells = kRegThreads * R;
+  __shared__ double edge_l[2][kWarps];  // first cell of each warp
+  __shared__ double edge_r[2][kWarps];  // last cell of each warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t valid = kCells - 2 * tb;
+  const int64_t t0 = (int64_t)blockIdx.x * valid - tb;  // global index of tile cell 0
+  const int64_t g0 = t0 + (int64_t)threadIdx.x * R;      // global index of my c[0]
+  const int64_t nn = (int64_t)n;
+
+  double c[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t g = g0 + i;
+    c[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
+  }
+  // does my range contain a global endpoint (0 or n-1)?  rare: slow path
+  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
+
+  for (int s = 0; s < tb; ++s) {
+    const int p = s & 1;
+    if (lane == 0) edge_l[p][warp] = c[0];
+    if (lane == 31) edge_r[p][warp] = c[R - 1];
+    double left = __shfl_up_sync(0xffffffffu, c[R - 1], 1);
+    double right = __shfl_down_sync(0xffffffffu, c[0], 1);
+    __syncthreads();
+    if (lane == 0) left = warp > 0 ? edge_r[p][warp - 1] : c[0];
+    if (lane == 31) right = warp < kWarps - 1 ? edge_l[p][warp + 1] : c[R - 1];
+    double prev = left;
+    if (!edge) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double nxt = (i + 1 < R) ? c[i + 1] : right;
+        const double v = point(prev, c[i], nxt);
+        prev = c[i];
+        c[i] = v;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double nxt = (i + 1 < R) ? c[i + 1] : right;
+        const int64_t g = g0 + i;
+        const double v = (g <= 0 || g >= nn - 1) ? c[i] : point(prev, c[i], nxt);
+        prev = c[i];
+        c[i] = v;
+      }
+    }
+  }
+  // write the valid centre [tb, kCells - tb) of the tile
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int local = threadIdx.x * R + i;
+    const int64_t g = g0 + i;
+    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = c[i];
+  }
+}
+
 }  // namespace
 
 extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t items,
@@ -120,14 +193,21 @@ extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n
   if (m) {
     const uint64_t npairs = (m + 1) >> 1;
     uint64_t blocks = (npairs + kThreads - 1) / kThreads;
-    const uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 8;
-    if (blocks > cap) blocks = cap;
     k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(x, y, n, m);
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return ofl::cuda_error(e, "stencil launch");
     ofl::count_launch();
   }
   return q.finish(ticket);
+}
+
+// heat pass kernel: 0 = register-blocked (default), 1 = shared-memory tiles
+static int heat_kernel() {
+  static int v = [] {
+    const char* e = getenv("OFL_HEAT_KERNEL");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
 }
 
 extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, int tb,
@@ -157,13 +237,17 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
     if (k == 1) {
       uint64_t npairs = (n + 1) >> 1;
       uint64_t blocks = (npairs + kThreads - 1) / kThreads;
-      if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
       k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(src, dst, n, n);
-    } else {
+    } else if (heat_kernel() == 1) {
       const uint64_t ntiles = (n + kTile - 1) / kTile;
       uint64_t blocks = ntiles < (uint64_t)sms * 2 ? ntiles : (uint64_t)sms * 2;
       const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
       k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
+    } else {
+      constexpr int R = 16;
+      const uint64_t valid = (uint64_t)kRegThreads * R - 2 * (uint64_t)k;
+      const uint64_t blocks = (n + valid - 1) / valid;
+      k_heat_reg<R><<<(unsigned)blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
     }
     ++launches;
     double* t = src;
