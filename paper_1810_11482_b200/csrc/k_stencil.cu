@@ -119,6 +119,37 @@ __global__ void __launch_bounds__(kTbThreads) k_heat_tb(const double* __restrict
 // which leaves the FP64 pipe (4 DP ops per cell-step) as the limiter.
 constexpr int kRegThreads = 256;
 
+// One step of the register tile: in[] -> out[] (distinct register arrays,
+// so an unrolled pair of steps needs no register moves).  Step parity p
+// selects the half of the warp-edge exchange buffer.
+template <int R>
+__device__ __forceinline__ void reg_step(const double (&in)[R], double (&out)[R],
+                                         double (*edge_l)[kRegThreads / 32],
+                                         double (*edge_r)[kRegThreads / 32], int p, int lane,
+                                         int warp, bool edge, int64_t g0, int64_t nn) {
+  constexpr int kWarps = kRegThreads / 32;
+  if (lane == 0) edge_l[p][warp] = in[0];
+  if (lane == 31) edge_r[p][warp] = in[R - 1];
+  double left = __shfl_up_sync(0xffffffffu, in[R - 1], 1);
+  double right = __shfl_down_sync(0xffffffffu, in[0], 1);
+  __syncthreads();
+  if (lane == 0) left = warp > 0 ? edge_r[p][warp - 1] : in[0];
+  if (lane == 31) right = warp < kWarps - 1 ? edge_l[p][warp + 1] : in[R - 1];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double l = i > 0 ? in[i - 1] : left;
+    const double r = i + 1 < R ? in[i + 1] : right;
+    out[i] = point(l, in[i], r);
+  }
+  if (edge) {  // rare: my cells include global cell 0 or n-1 (held fixed)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t g = g0 + i;
+      if (g <= 0 || g >= nn - 1) out[i] = in[i];
+    }
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restrict__ x,
                                                           double* __restrict__ y, uint64_t n,
@@ -133,50 +164,28 @@ __global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restri
   const int64_t g0 = t0 + (int64_t)threadIdx.x * R;      // global index of my c[0]
   const int64_t nn = (int64_t)n;
 
-  double c[R];
+  double a[R], b[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int64_t g = g0 + i;
-    c[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
+    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
   }
-  // does my range contain a global endpoint (0 or n-1)?  rare: slow path
+  // does my range contain a global endpoint (0 or n-1)?  rare
   const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
 
-  for (int s = 0; s < tb; ++s) {
-    const int p = s & 1;
-    if (lane == 0) edge_l[p][warp] = c[0];
-    if (lane == 31) edge_r[p][warp] = c[R - 1];
-    double left = __shfl_up_sync(0xffffffffu, c[R - 1], 1);
-    double right = __shfl_down_sync(0xffffffffu, c[0], 1);
-    __syncthreads();
-    if (lane == 0) left = warp > 0 ? edge_r[p][warp - 1] : c[0];
-    if (lane == 31) right = warp < kWarps - 1 ? edge_l[p][warp + 1] : c[R - 1];
-    double prev = left;
-    if (!edge) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const double nxt = (i + 1 < R) ? c[i + 1] : right;
-        const double v = point(prev, c[i], nxt);
-        prev = c[i];
-        c[i] = v;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const double nxt = (i + 1 < R) ? c[i + 1] : right;
-        const int64_t g = g0 + i;
-        const double v = (g <= 0 || g >= nn - 1) ? c[i] : point(prev, c[i], nxt);
-        prev = c[i];
-        c[i] = v;
-      }
-    }
+  int s = 0;
+  for (; s + 1 < tb; s += 2) {
+    reg_step<R>(a, b, edge_l, edge_r, 0, lane, warp, edge, g0, nn);
+    reg_step<R>(b, a, edge_l, edge_r, 1, lane, warp, edge, g0, nn);
   }
+  const bool odd = s < tb;
+  if (odd) reg_step<R>(a, b, edge_l, edge_r, 0, lane, warp, edge, g0, nn);
   // write the valid centre [tb, kCells - tb) of the tile
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int local = threadIdx.x * R + i;
     const int64_t g = g0 + i;
-    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = c[i];
+    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = odd ? b[i] : a[i];
   }
 }
 
@@ -206,6 +215,16 @@ static int heat_kernel() {
   static int v = [] {
     const char* e = getenv("OFL_HEAT_KERNEL");
     return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// cells per thread of the register-blocked kernel (8, 16 or 32)
+static int heat_cells_per_thread() {
+  static int v = [] {
+    const char* e = getenv("OFL_HEAT_R");
+    const int r = e ? atoi(e) : 8;  // profiles/r01_heat_sweep.txt
+    return (r == 16 || r == 32) ? r : 8;
   }();
   return v;
 }
@@ -244,10 +263,15 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
       const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
       k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
     } else {
-      constexpr int R = 16;
-      const uint64_t valid = (uint64_t)kRegThreads * R - 2 * (uint64_t)k;
-      const uint64_t blocks = (n + valid - 1) / valid;
-      k_heat_reg<R><<<(unsigned)blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
+      const int r = heat_cells_per_thread();
+      const uint64_t valid = (uint64_t)kRegThreads * r - 2 * (uint64_t)k;
+      const unsigned blocks = (unsigned)((n + valid - 1) / valid);
+      if (r == 8)
+        k_heat_reg<8><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
+      else if (r == 32)
+        k_heat_reg<32><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
+      else
+        k_heat_reg<16><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
     }
     ++launches;
     double* t = src;
