@@ -92,6 +92,11 @@ int ofl_host_free(void* hptr);
 int ofl_h2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
 int ofl_d2h(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
 int ofl_d2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
+/* H2D from pageable memory through a ring of pinned staging slots, the host
+ * copy of one chunk overlapping the DMA of the previous one; returns once the
+ * source has been fully staged (it may then be reused).  One ticket. */
+int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint64_t bytes,
+                     uint64_t* ticket);
 /* cross-device copy over NVLink (peer access enabled on first use) */
 int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev,
             uint64_t bytes, uint64_t* ticket);

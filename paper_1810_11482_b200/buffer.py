@@ -83,13 +83,10 @@ class BufferObject:
             if status:
                 raise_status(status, "write")
         else:
-            block = hostmem.pool.get(n)
-            hostmem.memcpy(block.addr, addr, n)
-            status = lib.ofl_h2d(st.ptr, dst, block.addr, n, ctypes.byref(ticket))
+            # pipelined multi-threaded staging in libofl (csrc/ofl_staging.cu)
+            status = lib.ofl_h2d_pageable(st.ptr, dst, addr, n, ctypes.byref(ticket))
             if status:
-                hostmem.pool.put(block)
                 raise_status(status, "write")
-            hostmem.free_block_later(st, ticket.value, block)
         return DeviceToken(st, ticket.value)
 
     def enqueue_read(self, offset: int, size: int, stream: int = 0) -> CompletionToken:

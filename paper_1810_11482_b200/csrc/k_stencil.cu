@@ -189,6 +189,160 @@ __global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restri
   }
 }
 
+// Warp-independent variant: every warp owns its own tile of 32*R cells
+// (halo tb each side, computed redundantly), so a step needs two shuffles
+// and no barrier at all; per-thread ILP (R independent cells) hides latency
+// instead of occupancy.
+constexpr int kWarpThreads = 128;
+
+template <int R>
+__device__ __forceinline__ void warp_step(const double (&in)[R], double (&out)[R], int lane,
+                                          bool edge, int64_t g0, int64_t nn) {
+  double left = __shfl_up_sync(0xffffffffu, in[R - 1], 1);
+  double right = __shfl_down_sync(0xffffffffu, in[0], 1);
+  if (lane == 0) left = in[0];
+  if (lane == 31) right = in[R - 1];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const double l = i > 0 ? in[i - 1] : left;
+    const double r = i + 1 < R ? in[i + 1] : right;
+    out[i] = point(l, in[i], r);
+  }
+  if (edge) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t g = g0 + i;
+      if (g <= 0 || g >= nn - 1) out[i] = in[i];
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __restrict__ x,
+                                                            double* __restrict__ y, uint64_t n,
+                                                            int tb) {
+  constexpr int kCells = 32 * R;
+  const int lane = threadIdx.x & 31;
+  const int64_t wtile = (int64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
+  const int64_t valid = kCells - 2 * tb;
+  const int64_t nn = (int64_t)n;
+  const int64_t g0 = wtile * valid - tb + (int64_t)lane * R;
+  if (wtile * valid >= nn) return;  // whole warp past the end (warp-uniform)
+  double a[R], b[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t g = g0 + i;
+    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
+  }
+  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
+  int s = 0;
+  for (; s + 1 < tb; s += 2) {
+    warp_step<R>(a, b, lane, edge, g0, nn);
+    warp_step<R>(b, a, lane, edge, g0, nn);
+  }
+  const bool odd = s < tb;
+  if (odd) warp_step<R>(a, b, lane, edge, g0, nn);
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int local = lane * R + i;
+    const int64_t g = g0 + i;
+    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = odd ? b[i] : a[i];
+  }
+}
+
+// Two-level temporal blocking.  Each warp runs warp-independent steps (two
+// shuffles, no barrier) on a warp tile of 32*R cells whose outer K cells on
+// each side are ghosts (K <= R/2, so they live in lanes 0 and 31); every K
+// steps the warps refresh their ghosts from their neighbours' boundary cells
+// through double-buffered shared memory (one barrier per K steps).  The
+// CTA's outer tb cells are the tile halo.  Redundant work drops from 2*tb per
+// warp (k_heat_warp) to 2*K per warp + 2*tb per CTA, barriers from one per
+// step (k_heat_reg) to one per K steps.
+constexpr int kHierWarps = 8;
+
+// lanes 0 / 31 publish their first / last K owned cells, barrier, then pull
+// the neighbours' into their ghosts (static register indices only)
+template <int R, int K>
+__device__ __forceinline__ void ghost_exchange(double (&c)[R], double (*sl)[K], double (*sr)[K],
+                                               int lane, int warp) {
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) sl[warp][i] = c[K + i];
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) sr[warp][i] = c[R - 2 * K + i];
+  }
+  __syncthreads();
+  if (lane == 0 && warp > 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) c[i] = sr[warp - 1][i];
+  }
+  if (lane == 31 && warp < kHierWarps - 1) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) c[R - K + i] = sl[warp + 1][i];
+  }
+}
+
+template <int R, int K>
+__global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __restrict__ x,
+                                                               double* __restrict__ y,
+                                                               uint64_t n, int tb) {
+  static_assert(2 * K <= R, "ghosts must fit in the edge lanes");
+  constexpr int kOwn = 32 * R - 2 * K;        // owned cells per warp
+  constexpr int kSpan = kHierWarps * kOwn;    // owned cells per CTA (incl. CTA halo)
+  __shared__ double sh_l[2][kHierWarps][K];   // each warp's first K owned cells
+  __shared__ double sh_r[2][kHierWarps][K];   // each warp's last K owned cells
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = (int64_t)n;
+  const int64_t cta0 = (int64_t)blockIdx.x * (kSpan - 2 * tb) - tb;  // global of CTA owned[0]
+  const int64_t g0 = cta0 + (int64_t)warp * kOwn - K + (int64_t)lane * R;  // my c[0]
+  double a[R], b[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t g = g0 + i;
+    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
+  }
+  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
+  int s = 0, ex = 0;
+  bool in_a = true;
+  while (s < tb) {
+    // K steps (or what is left) without any barrier
+    int k = 0;
+    for (; k + 1 < K && s + k + 1 < tb; k += 2) {
+      if (in_a) {
+        warp_step<R>(a, b, lane, edge, g0, nn);
+        warp_step<R>(b, a, lane, edge, g0, nn);
+      } else {
+        warp_step<R>(b, a, lane, edge, g0, nn);
+        warp_step<R>(a, b, lane, edge, g0, nn);
+      }
+    }
+    if (k < K && s + k < tb) {
+      if (in_a) warp_step<R>(a, b, lane, edge, g0, nn);
+      else warp_step<R>(b, a, lane, edge, g0, nn);
+      in_a = !in_a;
+      ++k;
+    }
+    s += k;
+    if (s >= tb) break;
+    // ghost refresh from the neighbouring warps
+    const int p = ex & 1;
+    ++ex;
+    if (in_a)
+      ghost_exchange<R, K>(a, sh_l[p], sh_r[p], lane, warp);
+    else
+      ghost_exchange<R, K>(b, sh_l[p], sh_r[p], lane, warp);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int own = warp * kOwn - K + lane * R + i;  // CTA owned coordinate
+    const int64_t g = g0 + i;
+    const bool mine = (lane * R + i >= K) && (lane * R + i < 32 * R - K);
+    if (mine && own >= tb && own < kSpan - tb && g >= 0 && g < nn) y[g] = in_a ? a[i] : b[i];
+  }
+}
+
 }  // namespace
 
 extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t items,
@@ -262,6 +416,21 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
       uint64_t blocks = ntiles < (uint64_t)sms * 2 ? ntiles : (uint64_t)sms * 2;
       const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
       k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
+    } else if (heat_kernel() == 3) {
+      constexpr int R = 16, K = 8;
+      const uint64_t span = (uint64_t)kHierWarps * (32 * R - 2 * K);
+      const uint64_t valid = span - 2 * (uint64_t)k;
+      const unsigned blocks = (unsigned)((n + valid - 1) / valid);
+      k_heat_hier<R, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k);
+    } else if (heat_kernel() == 2) {
+      const int r = heat_cells_per_thread();
+      const uint64_t valid = 32ull * r - 2 * (uint64_t)k;
+      const uint64_t warps = (n + valid - 1) / valid;
+      const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
+      if (r == 32)
+        k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
+      else
+        k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
     } else {
       const int r = heat_cells_per_thread();
       const uint64_t valid = (uint64_t)kRegThreads * r - 2 * (uint64_t)k;

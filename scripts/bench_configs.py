@@ -240,6 +240,36 @@ def overhead_cfg(rt, dev, out):
     out["config5_overhead"] = sweep
 
 
+def transfer_cfg(rt, dev, out):
+    """Host<->device copy rates through the API (enqueue_write/read)."""
+    n = 1 << 28  # 256 MiB
+    buf = dev.create_buffer(n).get()
+    buf2 = dev.create_buffer(n).get()
+    pin = pinned_empty(n)
+    pin2 = pinned_empty(n)
+    pin[:] = 7
+    page = np.full(n, 5, np.uint8)
+    res = {}
+
+    def rate(fn, reps=5):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return round(n * reps / (time.perf_counter() - t0) / 1e9, 2)
+
+    res["h2d_pinned_gbs"] = rate(lambda: buf.enqueue_write(0, pin).get())
+    res["d2h_pinned_gbs"] = rate(lambda: buf.enqueue_read_into(0, pin2).get())
+    s1 = dev.create_stream()
+    res["bidir_pinned_gbs_total"] = round(2 * rate(
+        lambda: when_all([buf.enqueue_write(0, pin), buf2.enqueue_read_into(0, pin2, s1)]).get()), 2)
+    res["h2d_pageable_numpy_gbs"] = rate(lambda: buf.enqueue_write(0, page).get())
+    res["d2h_to_bytes_gbs"] = rate(lambda: buf.enqueue_read(0, n).get(), reps=3)
+    ok = buf.enqueue_read(0, 4096).get() == bytes([5]) * 4096
+    res["pageable_roundtrip_ok"] = ok
+    out["transfers_256MiB"] = res
+
+
 def partition_cfg(rt, dev, out):
     res = {}
     for m in (1, 2, 3, 6):
@@ -264,7 +294,7 @@ def partition_cfg(rt, dev, out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="stream,heat,mandel,dot,overhead,partition")
+    ap.add_argument("--only", default="stream,heat,mandel,dot,overhead,partition,transfer")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     with open(os.path.join(REPO, "tests", "golden", "golden.json")) as fh:
@@ -280,7 +310,8 @@ def main():
              "mandel": lambda: mandel_cfg(rt, dev, out, golden),
              "dot": lambda: dot_cfg(rt, dev, out),
              "overhead": lambda: overhead_cfg(rt, dev, out),
-             "partition": lambda: partition_cfg(rt, dev, out)}[name]()
+             "partition": lambda: partition_cfg(rt, dev, out),
+             "transfer": lambda: transfer_cfg(rt, dev, out)}[name]()
             print(f"[{name}] {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
     text = json.dumps(out, indent=1)
     print(text)

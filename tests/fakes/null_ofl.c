@@ -68,3 +68,4 @@ int ofl_jit_compile(int d, const char* s, const char* e, void** o, char* l, int 
 int ofl_jit_launch(void* s, void* k, void** p, uint64_t b, int t, uint64_t* tk) { (void)k; (void)p; (void)b; (void)t; return op(s, tk); }
 int ofl_jit_destroy(void* k) { (void)k; return 0; }
 int ofl_fill_ones(void* s, void* d, uint64_t n, uint64_t* t) { memset(d, 0xff, n); return op(s, t); }
+int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
