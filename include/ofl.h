@@ -97,6 +97,8 @@ int ofl_d2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t*
  * source has been fully staged (it may then be reused).  One ticket. */
 int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint64_t bytes,
                      uint64_t* ticket);
+/* host-to-host copy on the library's copy threads (staging <-> pageable) */
+int ofl_host_memcpy(void* dst, const void* src, uint64_t bytes);
 /* cross-device copy over NVLink (peer access enabled on first use) */
 int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev,
             uint64_t bytes, uint64_t* ticket);

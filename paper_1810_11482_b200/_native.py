@@ -64,6 +64,7 @@ _SIGNATURES = {
     "ofl_d2h": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_d2d": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_h2d_pageable": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
+    "ofl_host_memcpy": (c_int, [c_void_p, c_void_p, c_uint64]),
     "ofl_p2p": (c_int, [_c_stream, c_void_p, c_int, c_void_p, c_int, c_uint64, _u64p]),
     "ofl_stream_wait": (c_int, [_c_stream, _c_stream, c_uint64]),
     "ofl_query": (c_int, [_c_stream, c_uint64, POINTER(c_int)]),

@@ -155,15 +155,16 @@ class _Landing:
         if self.into:
             hostmem.memcpy(self.into, self.block.addr, self.size)
             return None
-        return bytes(self.block.array[: self.size])
+        return hostmem.bytes_from(self.block.addr, self.size)
 
     def take(self):
+        # only called once the copy is complete (token finish), so the block
+        # can go back to the pool right away
         with self.lock:
             if not self.taken:
                 self.data = self._extract()
                 self.taken = True
-            if self.purged:
-                self._recycle()
+            self._recycle()
             data, self.data = self.data, None
         return data
 

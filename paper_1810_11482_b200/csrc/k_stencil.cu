@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __rest
 // CTA's outer tb cells are the tile halo.  Redundant work drops from 2*tb per
 // warp (k_heat_warp) to 2*K per warp + 2*tb per CTA, barriers from one per
 // step (k_heat_reg) to one per K steps.
-constexpr int kHierWarps = 8;
+constexpr int kHierWarps = 4;
 
 // lanes 0 / 31 publish their first / last K owned cells, barrier, then pull
 // the neighbours' into their ghosts (static register indices only)
@@ -364,21 +364,25 @@ extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n
   return q.finish(ticket);
 }
 
-// heat pass kernel: 0 = register-blocked (default), 1 = shared-memory tiles
+// heat pass kernel (OFL_HEAT_KERNEL): 2 = warp-independent register tiles
+// (default, fastest measured), 0 = CTA register tiles with a barrier per
+// step, 1 = shared-memory tiles, 3 = two-level (warp ghosts + CTA halo)
 static int heat_kernel() {
   static int v = [] {
     const char* e = getenv("OFL_HEAT_KERNEL");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
 
-// cells per thread of the register-blocked kernel (8, 16 or 32)
+// cells per thread of the register kernels (OFL_HEAT_R: 8, 16, 24, 32);
+// default per kernel from profiles/r01_heat_sweep.txt
 static int heat_cells_per_thread() {
   static int v = [] {
     const char* e = getenv("OFL_HEAT_R");
-    const int r = e ? atoi(e) : 8;  // profiles/r01_heat_sweep.txt
-    return (r == 16 || r == 32) ? r : 8;
+    const int dflt = heat_kernel() == 2 ? 24 : 8;
+    const int r = e ? atoi(e) : dflt;
+    return (r == 8 || r == 16 || r == 24 || r == 32) ? r : dflt;
   }();
   return v;
 }
@@ -429,6 +433,8 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
       const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
       if (r == 32)
         k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
+      else if (r == 24)
+        k_heat_warp<24><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
       else
         k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
     } else {

@@ -104,6 +104,19 @@ CopyPool& pool() {
 
 }  // namespace
 
+// Host memcpy on the copy pool (large staging <-> pageable copies).
+extern "C" int ofl_host_memcpy(void* dst, const void* src, uint64_t bytes) {
+  if (bytes >= (4u << 20)) {
+    static std::mutex mu;  // the pool runs one fork-join copy at a time
+    std::lock_guard<std::mutex> g(mu);
+    std::lock_guard<std::mutex> r(g_ring.mu);
+    pool().copy(dst, src, (size_t)bytes);
+  } else if (bytes) {
+    std::memcpy(dst, src, (size_t)bytes);
+  }
+  return OFL_OK;
+}
+
 extern "C" int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint64_t bytes,
                                 uint64_t* ticket) {
   OFL_CHECK_STREAM(s);

@@ -213,9 +213,22 @@ def writable_view(out) -> tuple[int, int, object]:
 
 
 def memcpy(dst: int, src: int, nbytes: int) -> None:
-    """Host copy (ctypes.memmove releases the GIL)."""
-    if nbytes:
+    """Host copy; large ones run on libofl's copy threads (GIL released)."""
+    if nbytes >= (4 << 20):
+        _native.load().ofl_host_memcpy(dst, src, nbytes)
+    elif nbytes:
         ctypes.memmove(dst, src, nbytes)
+
+
+def bytes_from(addr: int, nbytes: int) -> bytes:
+    """A new bytes object holding [addr, addr+nbytes): allocated zeroed
+    (calloc-backed for large sizes) and filled in place before anyone else
+    can see it — one copy, on the copy threads."""
+    if nbytes < (4 << 20) or not _BYTES_OFF:
+        return ctypes.string_at(addr, nbytes)
+    out = bytes(nbytes)
+    memcpy(id(out) + _BYTES_OFF, addr, nbytes)
+    return out
 
 
 def free_block_later(stream, ticket: int, block: Optional[Block]) -> None:

@@ -28,6 +28,28 @@ def main(which: str, reps: int = 3):
             p.build("triad").get()
             for _ in range(reps):
                 p.run([A, B, C, 3.0, n], "triad", (n // 256, 1, 1), (256, 1, 1))
+        elif which == "heat_time":  # tuning sweeps: config 2 timed, no oracle
+            import ctypes
+
+            from paper_1810_11482_b200 import _native
+
+            lib = _native.load()
+            n = 1 << 28
+            X, Y = d.create_buffer(n * 8).get(), d.create_buffer(n * 8).get()
+            X.enqueue_write(0, np.random.default_rng(0).random(n))
+            p = d.create_builtin_program().get()
+            p.build("heat").get()
+            p.run([X, Y, n, 64], "heat", (n // 256, 1, 1), (256, 1, 1))
+            st = rt.device_objects()[0].stream(0)
+            e0, e1 = ctypes.c_void_p(), ctypes.c_void_p()
+            lib.ofl_event_create(0, ctypes.byref(e0))
+            lib.ofl_event_create(0, ctypes.byref(e1))
+            lib.ofl_event_record(e0, st.ptr)
+            p.run([X, Y, n, 1000], "heat", (n // 256, 1, 1), (256, 1, 1))
+            lib.ofl_event_record(e1, st.ptr)
+            ms = ctypes.c_float()
+            lib.ofl_event_elapsed_ms(e0, e1, ctypes.byref(ms))
+            print(f"heat 2^28 x 1000 steps: {ms.value:.2f} ms")
         elif which in ("stencil", "heat"):
             n = 1 << 28
             X, Y = d.create_buffer(n * 8).get(), d.create_buffer(n * 8).get()

@@ -69,3 +69,4 @@ int ofl_jit_launch(void* s, void* k, void** p, uint64_t b, int t, uint64_t* tk) 
 int ofl_jit_destroy(void* k) { (void)k; return 0; }
 int ofl_fill_ones(void* s, void* d, uint64_t n, uint64_t* t) { memset(d, 0xff, n); return op(s, t); }
 int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
+int ofl_host_memcpy(void* d, const void* s, uint64_t n) { memcpy(d, s, n); return 0; }
