@@ -449,7 +449,7 @@ def run_ours(args) -> None:
                 "frac": round(achieved / peak, 4),
                 "traffic": traffic,
                 "peak_source": peak_src,
-                "kernel": "k_stream_vec<TRIAD> (csrc/k_stream.cu)",
+                "kernel": "k_stream_tile<TRIAD,512,1> (csrc/k_stream.cu)",
                 "algorithmic_bytes_per_launch": step_bytes,
                 "avg_launch_us": round(avg_launch_ms * 1e3, 3),
             },

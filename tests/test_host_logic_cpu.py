@@ -1,0 +1,117 @@
+"""Host-side logic of the CUDA runtime on CPU: handles, dispatch, argument
+validation, bindings' out-of-bounds pre-checks, device tokens and when_all
+over device tokens — driven against the null test double of libofl.so
+(tests/fakes/null_ofl.c: same C-ABI, no device, every op completes at once).
+Runs in a subprocess so the double never leaks into this process's
+libofl handle; the product path never loads it on its own."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAKE_SRC = os.path.join(REPO, "tests", "fakes", "null_ofl.c")
+FAKE_LIB = os.path.join(REPO, "tests", "fakes", "_build", "libnull_ofl.so")
+
+SCRIPT = textwrap.dedent(
+    r"""
+    import sys
+    sys.path.insert(0, REPO_PATH)
+    import numpy as np
+    from paper_1810_11482_b200 import (Runtime, when_all, make_ready, BadArgsError,
+        LaunchConfigError, NotBuiltError, OobAccessError, CompileError, UnknownGidError)
+    from paper_1810_11482_b200.bindings import kernel_source
+
+    def raises(exc, fn):
+        try:
+            fn()
+        except exc:
+            return
+        raise AssertionError(f"{exc.__name__} not raised")
+
+    with Runtime(devices=[0, 0]) as rt:
+        d0, d1 = rt.get_all_devices().get()
+        assert d0.info.name == "cuda0" and d0.info.capability == (10, 0)
+        assert d0.create_stream() == 1 and d0.create_stream() == 2
+        raises(BadArgsError, lambda: d0.create_buffer(0))
+        buf = d0.create_buffer(64).get()
+        raises(OobAccessError, lambda: buf.enqueue_write(60, b"12345"))
+        raises(BadArgsError, lambda: buf.enqueue_read(-1, 1))
+        buf.enqueue_write(0, b"abcdefgh")
+        assert buf.enqueue_read(0, 8).get() == b"abcdefgh"   # fake copies synchronously
+        out = bytearray(4)
+        buf.enqueue_read_into(2, out).get()
+        assert bytes(out) == b"cdef"
+
+        p = d0.create_program_with_source(kernel_source("sum")).get()
+        raises(NotBuiltError, lambda: p.run([buf, buf, 1], "sum", (1,1,1), (1,1,1)).get())
+        p.build("sum").get()
+        raises(BadArgsError, lambda: p.run([buf], "sum", (1,1,1), (1,1,1)).get())
+        raises(BadArgsError, lambda: p.run([buf, 3, buf], "sum", (1,1,1), (1,1,1)).get())
+        raises(BadArgsError, lambda: p.run([buf, buf, 2**32], "sum", (1,1,1), (1,1,1)))
+        raises(BadArgsError, lambda: p.run([buf, buf, True], "sum", (1,1,1), (1,1,1)))
+        raises(LaunchConfigError, lambda: p.run([buf, buf, 1], "sum", (0,1,1), (1,1,1)))
+        raises(LaunchConfigError, lambda: p.run([buf, buf, 1], "sum", (2**20,1,1), (2**13,1,1)))
+        other = d1.create_buffer(8).get()
+        raises(BadArgsError, lambda: p.run([other, buf, 1], "sum", (1,1,1), (1,1,1)))
+        # sum reading 17 words from a 16-word buffer: OOB at index 16
+        raises(OobAccessError, lambda: p.run([buf, buf, 17], "sum", (1,1,1), (1,1,1)).get())
+        p.run([buf, buf, 16], "sum", (1,1,1), (1,1,1)).get()
+
+        s = d0.create_program_with_source(kernel_source("stencil")).get()
+        s.build("stencil").get()
+        x = d0.create_buffer(99 * 8).get()
+        y = d0.create_buffer(100 * 8).get()
+        try:
+            s.run([x, y, 100], "stencil", (4,1,1), (32,1,1)).get()
+        except OobAccessError as e:
+            assert "index 99 " in str(e), e
+        else:
+            raise AssertionError("no OOB")
+        raises(BadArgsError, lambda: s.run([y, y, 100], "stencil", (4,1,1), (32,1,1)).get())
+
+        q = d0.create_program_with_source("kernel k(x : buffer_f64) { x[0] = nope; }").get()
+        raises(CompileError, lambda: q.build("k").get())
+
+        # device tokens + when_all chains (summarised per stream)
+        prev = make_ready(None)
+        toks = []
+        for i in range(2000):
+            w = buf.enqueue_write(0, bytes([i % 256]) * 8, i % 3)
+            toks.append(w)
+            prev = when_all([prev, w])
+        assert prev.get() is None and all(t.done() for t in toks)
+        fired = []
+        when_all(toks[-5:]).then(lambda _: fired.append(1))
+        import time
+        t0 = time.time()
+        while not fired and time.time() - t0 < 5:
+            time.sleep(0.01)
+        assert fired, "continuation never fired"
+        assert d0.synchronize().get() is None
+
+        rt.registry.unregister(buf.gid)
+        raises(UnknownGidError, lambda: buf.enqueue_read(0, 1).get())
+    print("HOST-LOGIC OK")
+    """
+)
+
+
+@pytest.fixture(scope="module")
+def fake_lib():
+    os.makedirs(os.path.dirname(FAKE_LIB), exist_ok=True)
+    subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-o", FAKE_LIB, FAKE_SRC], check=True)
+    return FAKE_LIB
+
+
+def test_host_logic_against_null_abi(fake_lib):
+    env = dict(os.environ, OFL_LIB=fake_lib)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.replace("REPO_PATH", repr(REPO))], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "HOST-LOGIC OK" in r.stdout
