@@ -228,7 +228,7 @@ def workload_config(n: int, world: int) -> dict:
     }
 
 
-def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int) -> dict:
+def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int, payload_bytes: int = 8) -> dict:
     """Per-future overhead vs raw CUDA streams (BASELINE config 5)."""
     import numpy as np
 
@@ -240,7 +240,7 @@ def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int) -> dict:
     A, B, C, D = (dev.create_buffer(n * 8).get() for _ in range(4))
     prog = dev.create_program_with_source(kernel_source("stream")).get()
     prog.build("triad").get()
-    payload = pinned_empty(8)
+    payload = pinned_empty(payload_bytes)
     payload[:] = 1
     args = [A, B, C, 3.0, n]
     grid, block = ((n + 255) // 256, 1, 1), (256, 1, 1)
@@ -252,7 +252,8 @@ def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int) -> dict:
         secs = ctypes.c_double()
         _native.check(
             lib.ofl_bench_raw_chain(
-                stream.ptr, dptr, payload.ctypes.data, 8, aptr, bptr, cptr, n, steps, mode,
+                stream.ptr, dptr, payload.ctypes.data, payload_bytes, aptr, bptr, cptr, n, steps,
+                mode,
                 ctypes.byref(secs),
             ),
             "raw chain",

@@ -74,12 +74,13 @@ class Stream:
     """One CUDA stream plus host objects that must outlive its in-flight
     operations (pinned sources, staging blocks)."""
 
-    __slots__ = ("ptr", "lib", "device", "sid", "_keep")
+    __slots__ = ("ptr", "lib", "device", "sid", "_keep", "_purge_lock")
 
     def __init__(self, device: "DeviceObject", sid: int):
         self.lib = _native.load()
         self.device = device
         self.sid = sid
+        self._purge_lock = threading.Lock()
         p = ctypes.c_void_p()
         _native.check(self.lib.ofl_stream_create(device.ordinal, ctypes.byref(p)), "stream create")
         self.ptr = p.value
@@ -115,17 +116,17 @@ class Stream:
         keep = self._keep
         if not keep:
             return
-        done = self.lib.ofl_stream_done(self.ptr)
-        if keep[0][0] > done and len(keep) > 256:
-            # long pipelines without observers: advance the watermark
-            ready = ctypes.c_int(0)
-            self.lib.ofl_query(self.ptr, keep[0][0], ctypes.byref(ready))
+        released = []
+        with self._purge_lock:  # check-then-pop must not interleave
             done = self.lib.ofl_stream_done(self.ptr)
-        while keep and keep[0][0] <= done:
-            try:
-                _, rel = keep.popleft()
-            except IndexError:
-                return
+            if keep[0][0] > done and len(keep) > 256:
+                # long pipelines without observers: advance the watermark
+                ready = ctypes.c_int(0)
+                self.lib.ofl_query(self.ptr, keep[0][0], ctypes.byref(ready))
+                done = self.lib.ofl_stream_done(self.ptr)
+            while keep and keep[0][0] <= done:
+                released.append(keep.popleft()[1])
+        for rel in released:
             if callable(rel):
                 rel()
 

@@ -237,7 +237,33 @@ def overhead_cfg(rt, dev, out):
     for k in (1, 10, 100, 1000, 10000, 100000):
         r = overhead_sweep(dev, rt, k, min(k, 2000))
         sweep[str(k)] = r
+    sweep["4KiB_payload_10000"] = overhead_sweep(dev, rt, 10000, 1000, payload_bytes=4096)
     out["config5_overhead"] = sweep
+
+
+def sum_cfg(rt, dev, out):
+    """u32 wrap-around sum (sum.k) at 2^28 elements: 4 B/elem, HBM-bound."""
+    st = rt.device_objects()[0].stream(0)
+    n = 1 << 28
+    v = np.random.default_rng(5).integers(0, 2**32, n, dtype=np.uint32)
+    I = dev.create_buffer(n * 4).get()
+    R = dev.create_buffer(4).get()
+    I.enqueue_write(0, v)
+    prog = dev.create_program_with_source(kernel_source("sum")).get()
+    prog.build("sum").get()
+    for _ in range(3):
+        prog.run([I, R, n], "sum", (1, 1, 1), (32, 1, 1))
+    t = Timer(st)
+    K = 50
+    t.start()
+    for _ in range(K):
+        prog.run([I, R, n], "sum", (1, 1, 1), (32, 1, 1))
+    ms = t.stop() / K
+    got = int(np.frombuffer(R.enqueue_read(0, 4).get(), np.uint32)[0])
+    gbs = 4.0 * n / (ms * 1e-3) / 1e9
+    out["sum_u32"] = {"n": n, "kernel_ms": round(ms, 4), "gbs": round(gbs, 1),
+                      "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
+                      "bitexact": got == oracle.sum_u32(v, threads=0)}
 
 
 def transfer_cfg(rt, dev, out):
@@ -294,7 +320,7 @@ def partition_cfg(rt, dev, out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="stream,heat,mandel,dot,overhead,partition,transfer")
+    ap.add_argument("--only", default="stream,heat,mandel,dot,sum,overhead,partition,transfer")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     with open(os.path.join(REPO, "tests", "golden", "golden.json")) as fh:
@@ -311,7 +337,8 @@ def main():
              "dot": lambda: dot_cfg(rt, dev, out),
              "overhead": lambda: overhead_cfg(rt, dev, out),
              "partition": lambda: partition_cfg(rt, dev, out),
-             "transfer": lambda: transfer_cfg(rt, dev, out)}[name]()
+             "transfer": lambda: transfer_cfg(rt, dev, out),
+             "sum": lambda: sum_cfg(rt, dev, out)}[name]()
             print(f"[{name}] {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
     text = json.dumps(out, indent=1)
     print(text)
