@@ -29,7 +29,7 @@ from functools import lru_cache
 from typing import Callable, Optional
 
 from . import _native
-from .errors import BadArgsError, OobAccessError
+from .errors import BadArgsError
 from .kernel import parse_and_validate
 from .kernel.canon import canonical
 
@@ -303,19 +303,6 @@ def _table() -> dict:
 
 def lookup(ir) -> Optional[Binding]:
     return _table().get(canonical(ir))
-
-
-def check_oob(binding: Binding, values: list, items: int) -> Optional[OobAccessError]:
-    if binding.oob is None:
-        return None
-    idx = binding.oob(values, items)
-    if idx is None:
-        return None
-    return OobAccessError(f"kernel buffer index {idx} out of range")
-
-
-def new_ticket():
-    return ctypes.c_uint64()
 
 
 _tls = threading.local()

@@ -162,14 +162,3 @@ class DeviceToken(CompletionToken):
             with _pending_lock:
                 _pending.pop(tid, None)
             self._fail(status, "completion notify failed")
-
-
-def wake(token: CompletionToken) -> None:
-    """Deliver a host-side token through the completion thread (used when a
-    continuation must not run on the caller's stack)."""
-    if isinstance(token, DeviceToken):
-        _ensure_thread()
-        tid = next(_ids)
-        with _pending_lock:
-            _pending[tid] = token
-        _native.load().ofl_completion_post(tid)

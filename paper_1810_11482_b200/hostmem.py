@@ -231,6 +231,3 @@ def bytes_from(addr: int, nbytes: int) -> bytes:
     return out
 
 
-def free_block_later(stream, ticket: int, block: Optional[Block]) -> None:
-    if block is not None:
-        stream.keep(ticket, lambda: pool.put(block))
