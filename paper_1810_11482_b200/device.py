@@ -25,6 +25,7 @@ from . import _native
 from .completion import DeviceToken
 from .errors import BadArgsError
 from .futures import CompletionToken, make_ready, when_all
+from .trace import Tracer
 
 DEFAULT_STREAM = 0
 
@@ -156,6 +157,7 @@ class DeviceObject:
         self.ordinal = physical.ordinal
         self.backend = "cuda"
         self.record_events = record_events
+        self.tracer = Tracer(self) if record_events else None
         self._lock = threading.Lock()
         self._streams: dict[int, Stream] = {}
         self._stream_ids = itertools.count(1)
@@ -209,6 +211,10 @@ class DeviceObject:
     @property
     def allocated_bytes(self) -> int:
         return self._allocated
+
+    def event_log(self) -> list:
+        """Traced operations (Runtime(record_events=True)); empty otherwise."""
+        return self.tracer.event_log() if self.tracer is not None else []
 
     def close(self) -> None:
         with self._lock:

@@ -80,21 +80,43 @@ class CudaDispatch:
 
         return self._tokenized(start)
 
+    @staticmethod
+    def _traced(dev, stream, op, amount, fn):
+        """Run one enqueue, bracketed by trace events when the device records
+        events (Runtime(record_events=True); reference device.py:330-350)."""
+        tr = dev.tracer
+        if tr is None:
+            return fn()
+        st = dev.stream(stream)
+        e0 = tr.begin(st)
+        tok = fn()
+        tr.end(st, e0, op, amount)
+        return tok
+
     def write(self, buffer_gid, offset, data, stream, device=None) -> CompletionToken:
         try:
-            return self._buffer(buffer_gid).enqueue_write(offset, data, stream)
+            buf = self._buffer(buffer_gid)
+            if buf.device.tracer is None:
+                return buf.enqueue_write(offset, data, stream)
+            n = memoryview(data).nbytes if not isinstance(data, bytes) else len(data)
+            return self._traced(buf.device, stream, "write", n,
+                                lambda: buf.enqueue_write(offset, data, stream))
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 
     def read(self, buffer_gid, offset, size, stream, device=None) -> CompletionToken:
         try:
-            return self._buffer(buffer_gid).enqueue_read(offset, size, stream)
+            buf = self._buffer(buffer_gid)
+            return self._traced(buf.device, stream, "read", size,
+                                lambda: buf.enqueue_read(offset, size, stream))
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 
     def read_into(self, buffer_gid, offset, out, stream, device=None) -> CompletionToken:
         try:
-            return self._buffer(buffer_gid).enqueue_read_into(offset, out, stream)
+            buf = self._buffer(buffer_gid)
+            return self._traced(buf.device, stream, "read", memoryview(out).nbytes,
+                                lambda: buf.enqueue_read_into(offset, out, stream))
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 
@@ -144,11 +166,13 @@ class CudaDispatch:
             program = self._program(program_gid)
             if items is None:
                 items = launch_items(grid, block)
-            resolved = [
-                ("buffer", self._buffer(value)) if tag == "buffer" else (tag, value)
-                for tag, value in args
-            ]
-            return program.run(kernel_name, items, stream, resolved, grid, block)
+            # buffer gids are resolved in the same pass as the kind checks
+            if program.device.tracer is None:
+                return program.run(kernel_name, items, stream, args, grid, block, self._buffer)
+            return self._traced(
+                program.device, stream, "run", items,
+                lambda: program.run(kernel_name, items, stream, args, grid, block, self._buffer),
+            )
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 

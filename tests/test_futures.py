@@ -172,3 +172,20 @@ def test_deep_when_all_chain_error():
     for i, p in enumerate(ps):
         if i != 5000:
             p.set_value(None)
+
+
+def test_gid_uniqueness_million():
+    from paper_1810_11482_b200.registry import ObjectKind, Registry
+
+    reg = Registry()
+    gids = {reg.register(ObjectKind.BUFFER, i) for i in range(1_000_000)}
+    assert len(gids) == 1_000_000
+    g = next(iter(gids))
+    assert reg.resolve_local(g, ObjectKind.BUFFER) is not None
+    reg.unregister(g)
+    import pytest as _p
+
+    from paper_1810_11482_b200.errors import UnknownGidError
+
+    with _p.raises(UnknownGidError):
+        reg.resolve_local(g)

@@ -1,0 +1,88 @@
+"""More API behaviour on the B200: tracing (reference event log), adversarial
+byte ranges (reference test_buffer.py hypothesis case), multi-device heat
+with a temporal-blocking halo, dot over two logical devices."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_1810_11482_b200 import OobAccessError, Runtime
+from paper_1810_11482_b200.bindings import kernel_source
+
+pytestmark = pytest.mark.gpu
+
+
+def test_event_log_records_ops_in_order():
+    with Runtime(devices=[0], record_events=True) as rt:
+        dev = rt.get_all_devices().get()[0]
+        obj = rt.device_objects()[0]
+        buf = dev.create_buffer(4096 * 8).get()
+        prog = dev.create_program_with_source(kernel_source("partition")).get()
+        prog.build("partition").get()
+        s1 = dev.create_stream()
+        buf.enqueue_write(0, bytes(4096 * 8), s1)
+        prog.run([buf, 0, 4096], "partition", (16, 1, 1), (256, 1, 1), s1)
+        buf.enqueue_read(0, 64, s1).get()
+        log = obj.event_log()
+        assert [e.op for e in log] == ["write", "run", "read"]
+        assert [e.amount for e in log] == [4096 * 8, 4096, 64]
+        assert all(e.engine == "cuda0-s1" and e.stream == s1 for e in log)
+        assert all(0 <= e.start <= e.end for e in log)
+        assert log[0].end <= log[1].start + 1e-3 and log[1].end <= log[2].start + 1e-3
+
+
+def test_event_log_empty_when_off(rt):
+    assert rt.device_objects()[0].event_log() == []
+
+
+_RT = {}
+
+
+def _dev():
+    if "rt" not in _RT:
+        _RT["rt"] = Runtime(devices=[0])
+    return _RT["rt"].get_all_devices().get()[0]
+
+
+@given(st.integers(0, 256), st.integers(0, 256), st.binary(max_size=256))
+@settings(max_examples=150, deadline=None)
+def test_adversarial_ranges_never_corrupt(offset, size, blob):
+    dev = _dev()
+    buf = dev.create_buffer(128).get()
+    try:
+        buf.enqueue_write(offset, blob)
+    except OobAccessError:
+        assert offset + len(blob) > 128
+    try:
+        data = buf.enqueue_read_sync(offset, size)
+        assert offset + size <= 128 and len(data) == size
+    except OobAccessError:
+        assert offset + size > 128
+
+
+@pytest.mark.parametrize("halo,steps", [(64, 200), (16, 50), (7, 22)])
+def test_heat_multi_device_temporal_halo(rt2, halo, steps):
+    from paper_1810_11482_b200.bench.harness import heat_multi
+
+    import oracle
+
+    devices = rt2.get_all_devices().get()
+    x = np.random.default_rng(halo).random(200_003)
+    got = heat_multi(devices, x, steps, halo=halo)
+    assert got.tobytes() == oracle.heat(x, steps, threads=0).tobytes()
+
+
+def test_dot_two_logical_devices_host_sum(rt2):
+    from paper_1810_11482_b200.bench.harness import dot_multi
+
+    import oracle
+
+    devices = rt2.get_all_devices().get()
+    a = np.random.default_rng(3).random(3_000_001, dtype=np.float32)
+    b = np.random.default_rng(4).random(3_000_001, dtype=np.float32)
+    got = dot_multi(devices, a, b)  # no NCCL across logical devices of one GPU
+    exp = oracle.dot_f32(a, b)
+    assert abs(got - exp) <= 1e-12 * abs(exp)
