@@ -100,6 +100,88 @@ __device__ __forceinline__ void escape_count2(double cra, double cia, double crb
   nb = cb;
 }
 
+// P pixels per thread in lock step (generalises escape_count2).
+template <bool INTCMP, int P>
+__device__ __forceinline__ void escape_countP(const double (&cr)[P], const double (&ci)[P],
+                                              double esc, uint32_t max_iter, uint32_t (&n)[P]) {
+  double zr[P], zi[P];
+  bool live[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    zr[p] = 0.0;
+    zi[p] = 0.0;
+    n[p] = 0;
+    live[p] = true;
+  }
+  const long long esc_bits = __double_as_longlong(esc);
+  for (uint32_t i = 0; i < max_iter; ++i) {
+    double r2[P], i2[P];
+    bool any = false;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      r2[p] = __dmul_rn(zr[p], zr[p]);
+      i2[p] = __dmul_rn(zi[p], zi[p]);
+      const double m = __dadd_rn(r2[p], i2[p]);
+      const bool out = INTCMP ? (__double_as_longlong(m) > esc_bits) : (m > esc);
+      live[p] = live[p] && !out;
+      any = any || live[p];
+    }
+    if (!any) break;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      n[p] += live[p];
+      const double t = __dadd_rn(__dsub_rn(r2[p], i2[p]), cr[p]);
+      zi[p] = __dadd_rn(__dmul_rn(__dmul_rn(2.0, zr[p]), zi[p]), ci[p]);
+      zr[p] = t;
+    }
+  }
+}
+
+// ILP-P variant: lane l handles the same position of the P tiles of a unit.
+template <bool INTCMP, int P>
+__global__ void __launch_bounds__(kThreads) k_mandelbrotP(MandelArgs a, unsigned int* queue) {
+  static_assert(kTilesPerUnit % P == 0, "P must divide the unit");
+  const int lane = threadIdx.x & 31;
+  const double dre = __dsub_rn(a.re1, a.re0);
+  const double dim = __dsub_rn(a.im1, a.im0);
+  const double fw = (double)a.width, fh = (double)a.height;
+  while (true) {
+    unsigned int u = 0;
+    if (lane == 0) u = atomicAdd(queue, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((uint64_t)u >= a.units) break;
+#pragma unroll 1
+    for (int k = 0; k < kTilesPerUnit; k += P) {
+      uint64_t at[P];
+      double cr[P], ci[P];
+      bool ok[P];
+      uint32_t cnt[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const uint64_t tile = (uint64_t)u * kTilesPerUnit + k + j;
+        const uint32_t ty = (uint32_t)(tile / a.tiles_x);
+        const uint32_t tx = (uint32_t)(tile % a.tiles_x);
+        const uint32_t px = tx * kTileW + (lane & (kTileW - 1));
+        const uint32_t r = ty * kTileH + (lane >> 3);
+        const uint32_t py = a.row_first + r * a.row_step;
+        const uint64_t gtid = (uint64_t)py * a.width + px;
+        ok[j] = r < a.rows && px < a.width && gtid < a.limit;
+        at[j] = a.compact ? (uint64_t)r * a.width + px : gtid;
+        const double c_re =
+            __dadd_rn(a.re0, __ddiv_rn(__dmul_rn(__dadd_rn((double)px, 0.5), dre), fw));
+        const double c_im =
+            __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
+        cr[j] = ok[j] ? c_re : 1e3;  // off-image lanes escape at once, never stored
+        ci[j] = ok[j] ? c_im : 0.0;
+      }
+      escape_countP<INTCMP, P>(cr, ci, a.esc, a.max_iter, cnt);
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        if (ok[j]) a.out[at[j]] = cnt[j];
+    }
+  }
+}
+
 // ILP-2 variant of k_mandelbrot: a unit is 4 tiles of 8x4; lane l handles
 // the same tile position in tiles (k, k+1) — pixels 8 apart, which escape
 // at similar counts.
@@ -228,7 +310,17 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
         const char* e = getenv("OFL_MANDEL_ILP");
         return e ? atoi(e) : 2;
       }();
-      if (ilp == 2) {
+      if (ilp == 4) {
+        if (intcmp)
+          k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+        else
+          k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      } else if (ilp == 3) {  // the generic template at P=2
+        if (intcmp)
+          k_mandelbrotP<true, 2><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+        else
+          k_mandelbrotP<false, 2><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      } else if (ilp == 2) {
         if (intcmp)
           k_mandelbrot2<true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
         else
