@@ -56,7 +56,10 @@ def _completion_loop(fd: int) -> None:
                 toks = [_pending.pop(buf[i], None) for i in range(n)]
             for tok in toks:
                 if tok is not None:
-                    tok._finish_now()
+                    try:
+                        tok._finish_now()
+                    except BaseException:  # noqa: BLE001 - a raw callback raised;
+                        pass  # the thread must survive to complete other tokens
 
 
 def _ensure_thread() -> None:

@@ -306,9 +306,11 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       const double lim = 1e10;
       const bool intcmp = esc > 0.0 && esc <= lim && fabs(re0) <= lim && fabs(re1) <= lim &&
                           fabs(im0) <= lim && fabs(im1) <= lim && getenv("OFL_MANDEL_FPCMP") == nullptr;
+      // pixels per thread in lock step (OFL_MANDEL_ILP 1/2/3/4); 4 measured
+      // fastest (profiles/r01_mandel_sweep.txt)
       static const int ilp = [] {
         const char* e = getenv("OFL_MANDEL_ILP");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 4;
       }();
       if (ilp == 4) {
         if (intcmp)
