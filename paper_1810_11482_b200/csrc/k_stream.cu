@@ -121,6 +121,74 @@ __global__ void __launch_bounds__(T) k_stream_tile(double* __restrict__ a,
   }
 }
 
+// TMA (bulk-copy engine) form: one elected thread moves each input tile
+// global->shared with cp.async.bulk completing on an mbarrier, the CTA
+// computes in shared memory (in place over b), and the tile goes back with
+// one shared->global bulk store.  Tiles of kTmaTile doubles per input.
+constexpr int kTmaThreads = 256;
+constexpr int kTmaTile = 2048;  // 16 KiB per input tile
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int OP, int TILE = kTmaTile>
+__global__ void __launch_bounds__(kTmaThreads) k_stream_tma(double* __restrict__ a,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ c,
+                                                          double s, uint64_t n) {
+  constexpr bool kC = (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD);
+  __shared__ alignas(128) double sb[TILE];
+  __shared__ alignas(128) double sc[kC ? TILE : 1];
+  __shared__ alignas(8) uint64_t bar;
+  const uint64_t base = (uint64_t)blockIdx.x * TILE;
+  const uint64_t count = n - base < (uint64_t)TILE ? n - base : (uint64_t)TILE;
+  const uint32_t bytes = (uint32_t)(count * 8) & ~15u;  // bulk sizes are 16-byte multiples
+  const uint32_t bar_a = smem_u32(&bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a),
+                 "r"(kC ? 2 * bytes : bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(sb)), "l"(b + base), "r"(bytes), "r"(bar_a)
+        : "memory");
+    if constexpr (kC)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(sc)), "l"(c + base), "r"(bytes), "r"(bar_a)
+          : "memory");
+  }
+  if (bytes) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar_a)
+          : "memory");
+  }
+  const uint32_t m = bytes / 8;  // elements covered by the bulk copies
+  for (uint32_t i = threadIdx.x; i < m; i += kTmaThreads)
+    sb[i] = apply<OP>(sb[i], kC ? sc[i] : 0.0, s);
+  for (uint64_t i = base + m + threadIdx.x; i < base + count; i += kTmaThreads)
+    a[i] = apply<OP>(b[i], kC ? c[i] : 0.0, s);  // < 2 leftover elements
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a + base),
+                 "r"(smem_u32(sb)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 // Fallback for operands that are not 16-byte aligned.
 template <int OP>
 __global__ void __launch_bounds__(kThreads) k_stream_scalar(double* a, const double* b,
@@ -187,6 +255,16 @@ cudaError_t launch(cudaStream_t st, int sms, double* a, const double* b, const d
     case 13: launch_tile<OP, 1024, 1>(st, a, b, c, s, n); break;
     case 14: launch_tile<OP, 128, 4>(st, a, b, c, s, n); break;
     case 15: launch_tile<OP, 128, 2>(st, a, b, c, s, n); break;
+    case 16: {
+      const uint64_t blocks = (n + 2047) / 2048;
+      k_stream_tma<OP, 2048><<<(unsigned)(blocks ? blocks : 1), kTmaThreads, 0, st>>>(a, b, c, s, n);
+      break;
+    }
+    case 17: {
+      const uint64_t blocks = (n + 1023) / 1024;
+      k_stream_tma<OP, 1024><<<(unsigned)(blocks ? blocks : 1), kTmaThreads, 0, st>>>(a, b, c, s, n);
+      break;
+    }
     default:
       // measured best on B200 (profiles/r01_stream_sweep.txt): one-shot tiles,
       // 512 threads; 1 double2 per input per thread for the 2-input ops,
