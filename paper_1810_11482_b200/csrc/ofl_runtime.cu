@@ -428,14 +428,27 @@ int ofl_wait(ofl_stream* s, uint64_t ticket) {
   OFL_CHECK_STREAM(s);
   if (ticket == 0 || s->done.load(std::memory_order_acquire) >= ticket) return OFL_OK;
   std::shared_ptr<EvBox> box;
+  uint64_t tail_sync = 0;
   {
     std::lock_guard<std::mutex> g(s->mu);
     if (ticket > s->tail) return set_error(OFL_ERR_BAD_ARGS, "ticket not yet enqueued");
     int st = reap(s);
     if (st) return st;
     if (s->done.load() >= ticket) return OFL_OK;
-    st = covering(s, ticket, &box);
-    if (st) return st;
+    if (ticket == s->tail && (s->markers.empty() || s->markers.back()->ticket < ticket)) {
+      tail_sync = s->tail;  // waiting on the newest op: no marker needed
+    } else {
+      st = covering(s, ticket, &box);
+      if (st) return st;
+    }
+  }
+  if (tail_sync) {
+    cudaError_t e = use_device(s->dev);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->cs);
+    if (e != cudaSuccess) return cuda_error(e, "device fault");
+    raise_done(s, tail_sync);
+    std::lock_guard<std::mutex> g(s->mu);
+    return reap(s);
   }
   cudaError_t e = cudaEventSynchronize(box->ev);
   if (e != cudaSuccess) return cuda_error(e, "device fault");
