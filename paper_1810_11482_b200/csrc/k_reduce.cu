@@ -12,6 +12,8 @@
 //   - fp64 partials are folded in a fixed order for a given grid, so the dot
 //     result is run-to-run deterministic; each fp32*fp32 product is exact in
 //     fp64, only the accumulation rounds.
+#include <cstdlib>
+
 #include "ofl_internal.h"
 
 namespace {
@@ -19,11 +21,16 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kMaxBlocks = 148 * 4;
 
+// Lives at kScratchOffset of the per-stream scratch (the Mandelbrot work
+// queue uses offset 32768); `partial` has one slot per CTA of the launch.
+constexpr size_t kScratchOffset = 65536;
 struct Scratch {
   unsigned int counter;
   unsigned int pad[63];
-  uint64_t partial[kMaxBlocks];  // u32 sums or fp64 bit patterns
+  uint64_t partial[1];  // u32 sums or fp64 bit patterns, gridDim.x of them
 };
+
+size_t scratch_bytes(uint64_t blocks) { return kScratchOffset + 256 + 8 * blocks; }
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
@@ -141,13 +148,22 @@ __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ 
   if (fold<double>(sc, acc, &total)) res[0] = total;
 }
 
-int grid_for(ofl_stream* s, uint64_t vec_units) {
-  uint64_t blocks = (vec_units + kThreads * 4 - 1) / (kThreads * 4);
+// Grid: persistent, 4 CTAs (2048 threads, full occupancy) per SM with a
+// grid-stride loop. A one-shot grid (one unrolled round per thread) measured
+// slower on B200 — 0.198 vs 0.167 ms for sum 2^28, 3.46 vs 2.60 ms for dot
+// 2^31 (profiles/r01_reduce_grid.txt): the per-CTA atomic ticket and the
+// last CTA's fold over ~10^5 partials cost more than the tail it balances.
+int grid_for(ofl_stream* s, uint64_t vec_units, int unroll) {
+  uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
   uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 4;
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   return (int)blocks;
+}
+
+Scratch* reduce_scratch(void* base) {
+  return reinterpret_cast<Scratch*>(static_cast<char*>(base) + kScratchOffset);
 }
 
 }  // namespace
@@ -159,11 +175,11 @@ extern "C" int ofl_sum_u32(ofl_stream* s, const uint32_t* in, uint32_t* res, uin
     return ofl::set_error(OFL_ERR_BAD_ARGS, "sum input must be 16-byte aligned");
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
+  const int blocks = grid_for(s, n >> 2, 4);
   void* scratch = nullptr;
-  int st = ofl::stream_scratch(s, sizeof(Scratch), &scratch);
+  int st = ofl::stream_scratch(s, scratch_bytes(blocks), &scratch);
   if (st) return st;
-  k_sum_u32<<<grid_for(s, n >> 2), kThreads, 0, s->cs>>>(in, res, n,
-                                                          static_cast<Scratch*>(scratch));
+  k_sum_u32<<<blocks, kThreads, 0, s->cs>>>(in, res, n, reduce_scratch(scratch));
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return ofl::cuda_error(e, "sum launch");
   ofl::count_launch();
@@ -177,11 +193,11 @@ extern "C" int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double
     return ofl::set_error(OFL_ERR_BAD_ARGS, "dot operands must be 16-byte aligned");
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
+  const int blocks = grid_for(s, n >> 2, 2);
   void* scratch = nullptr;
-  int st = ofl::stream_scratch(s, sizeof(Scratch), &scratch);
+  int st = ofl::stream_scratch(s, scratch_bytes(blocks), &scratch);
   if (st) return st;
-  k_dot_f32<<<grid_for(s, n >> 2), kThreads, 0, s->cs>>>(a, b, res, n,
-                                                          static_cast<Scratch*>(scratch));
+  k_dot_f32<<<blocks, kThreads, 0, s->cs>>>(a, b, res, n, reduce_scratch(scratch));
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return ofl::cuda_error(e, "dot launch");
   ofl::count_launch();

@@ -43,6 +43,11 @@ __global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__
   {
     const uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
     const uint64_t lo = 2 * j;
+    // the warp-edge neighbours are loaded together with the main vector, so
+    // a warp waits for one memory latency, not two
+    double edge = 0.0;
+    if (lane == 0 && lo >= 1 && lo - 1 <= hi) edge = x[lo - 1];
+    if (lane == 31 && lo + 2 <= hi) edge = x[lo + 2];
     double2 v = make_double2(0.0, 0.0);
     if (lo + 1 <= hi) {
       v = __ldcs(reinterpret_cast<const double2*>(x) + j);
@@ -51,8 +56,8 @@ __global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__
     }
     double left = __shfl_up_sync(0xffffffffu, v.y, 1);
     double right = __shfl_down_sync(0xffffffffu, v.x, 1);
-    if (lane == 0 && lo >= 1 && lo - 1 <= hi) left = x[lo - 1];
-    if (lane == 31 && lo + 2 <= hi) right = x[lo + 2];
+    if (lane == 0) left = edge;
+    if (lane == 31) right = edge;
     if (lo < m) {
       const double r0 = (lo == 0 || lo == n - 1) ? v.x : point(left, v.x, v.y);
       if (lo + 1 < m) {
