@@ -200,20 +200,38 @@ __global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restri
 // instead of occupancy.
 constexpr int kWarpThreads = 128;
 
-template <int R>
+// Fused form of point(): when 0.5*l and 0.5*r are exact (no result below
+// 2^-1022), round(0.5*l + c) is exactly __dadd_rn(__dmul_rn(0.5, l), c), so
+//   (0.5*l + c) + 0.5*r  ==  fma(0.5, r, fma(0.5, l, c))      bit for bit
+// — two DFMA instead of DMUL + 2 DADD (3 after CSE).  Only valid under the
+// tile guard in k_heat_warp (heat_fma_safe).
+__device__ __forceinline__ double point_fma(double l, double c, double r) {
+  return __fma_rn(0.5, r, __fma_rn(0.5, l, c));
+}
+
+// One step of a warp tile.  kEdge: some lane holds global cell 0 or n-1
+// (held fixed), decided warp-uniformly so the common case has no per-step
+// test.  kClamp: lanes 0 / 31 use their own edge cell as the outer
+// neighbour; without it they read an arbitrary finite-or-not value, which
+// is harmless: garbage enters at the tile ends and moves one cell per step,
+// so after tb steps it has reached only the tb-cell halo that is never
+// written back (the valid cells' dependency cones lie inside the tile).
+template <int R, bool kFma, bool kEdge, bool kClamp = false>
 __device__ __forceinline__ void warp_step(const double (&in)[R], double (&out)[R], int lane,
-                                          bool edge, int64_t g0, int64_t nn) {
+                                          int64_t g0, int64_t nn) {
   double left = __shfl_up_sync(0xffffffffu, in[R - 1], 1);
   double right = __shfl_down_sync(0xffffffffu, in[0], 1);
-  if (lane == 0) left = in[0];
-  if (lane == 31) right = in[R - 1];
+  if (kClamp) {
+    if (lane == 0) left = in[0];
+    if (lane == 31) right = in[R - 1];
+  }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const double l = i > 0 ? in[i - 1] : left;
     const double r = i + 1 < R ? in[i + 1] : right;
-    out[i] = point(l, in[i], r);
+    out[i] = kFma ? point_fma(l, in[i], r) : point(l, in[i], r);
   }
-  if (edge) {
+  if (kEdge) {
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int64_t g = g0 + i;
@@ -222,10 +240,50 @@ __device__ __forceinline__ void warp_step(const double (&in)[R], double (&out)[R
   }
 }
 
+template <int R, bool kFma, bool kEdge>
+__device__ __forceinline__ bool warp_steps(double (&a)[R], double (&b)[R], int lane, int64_t g0,
+                                           int64_t nn, int tb) {
+  int s = 0;
+  for (; s + 1 < tb; s += 2) {
+    warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
+    warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
+  }
+  if (s < tb) warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
+  return s < tb;
+}
+
+// tb steps of a warp tile held in registers (a -> a or b; returns true when
+// the result is in b).  Tile guard for the fused update: every cell is +0 or
+// a positive number >= 2^(tb-1020) (inf/nan included).  With non-negative
+// inputs a cell never decreases and a new non-zero is at least half a
+// non-zero neighbour, so over tb steps every operand stays >= 2^-1020 or
+// zero and 0.5*x is exact.  Otherwise (signs, -0, tiny values) the warp takes
+// the unfused path.  The guard is warp-uniform (__all_sync).
+template <int R>
+__device__ __forceinline__ bool warp_tile_steps(double (&a)[R], double (&b)[R], int lane,
+                                                bool edge, int64_t g0, int64_t nn, int tb,
+                                                bool fma_ok) {
+  bool safe = fma_ok;
+  if (safe) {
+    const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
+      safe &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
+    }
+  }
+  safe = __all_sync(0xffffffffu, safe);
+  if (__any_sync(0xffffffffu, edge))
+    return safe ? warp_steps<R, true, true>(a, b, lane, g0, nn, tb)
+                : warp_steps<R, false, true>(a, b, lane, g0, nn, tb);
+  return safe ? warp_steps<R, true, false>(a, b, lane, g0, nn, tb)
+              : warp_steps<R, false, false>(a, b, lane, g0, nn, tb);
+}
+
 template <int R>
 __global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __restrict__ x,
                                                             double* __restrict__ y, uint64_t n,
-                                                            int tb) {
+                                                            int tb, bool fma_ok) {
   constexpr int kCells = 32 * R;
   const int lane = threadIdx.x & 31;
   const int64_t wtile = (int64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
@@ -240,13 +298,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __rest
     a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
   }
   const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
-  int s = 0;
-  for (; s + 1 < tb; s += 2) {
-    warp_step<R>(a, b, lane, edge, g0, nn);
-    warp_step<R>(b, a, lane, edge, g0, nn);
-  }
-  const bool odd = s < tb;
-  if (odd) warp_step<R>(a, b, lane, edge, g0, nn);
+  const bool odd = warp_tile_steps<R>(a, b, lane, edge, g0, nn, tb, fma_ok);
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int local = lane * R + i;
@@ -308,7 +360,6 @@ __global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __r
     const int64_t g = g0 + i;
     a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
   }
-  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
   int s = 0, ex = 0;
   bool in_a = true;
   while (s < tb) {
@@ -316,16 +367,16 @@ __global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __r
     int k = 0;
     for (; k + 1 < K && s + k + 1 < tb; k += 2) {
       if (in_a) {
-        warp_step<R>(a, b, lane, edge, g0, nn);
-        warp_step<R>(b, a, lane, edge, g0, nn);
+        warp_step<R, false, true, true>(a, b, lane, g0, nn);
+        warp_step<R, false, true, true>(b, a, lane, g0, nn);
       } else {
-        warp_step<R>(b, a, lane, edge, g0, nn);
-        warp_step<R>(a, b, lane, edge, g0, nn);
+        warp_step<R, false, true, true>(b, a, lane, g0, nn);
+        warp_step<R, false, true, true>(a, b, lane, g0, nn);
       }
     }
     if (k < K && s + k < tb) {
-      if (in_a) warp_step<R>(a, b, lane, edge, g0, nn);
-      else warp_step<R>(b, a, lane, edge, g0, nn);
+      if (in_a) warp_step<R, false, true, true>(a, b, lane, g0, nn);
+      else warp_step<R, false, true, true>(b, a, lane, g0, nn);
       in_a = !in_a;
       ++k;
     }
@@ -392,6 +443,16 @@ static int heat_cells_per_thread() {
   return v;
 }
 
+// fused two-DFMA update under the tile guard (OFL_HEAT_FMA=0 disables; the
+// unfused kernel is kept for the sweep and for tiles the guard rejects)
+static bool heat_fused() {
+  static bool v = [] {
+    const char* e = getenv("OFL_HEAT_FMA");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, int tb,
                         uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
@@ -433,15 +494,16 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
       k_heat_hier<R, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k);
     } else if (heat_kernel() == 2) {
       const int r = heat_cells_per_thread();
+      const bool fma = heat_fused();
       const uint64_t valid = 32ull * r - 2 * (uint64_t)k;
       const uint64_t warps = (n + valid - 1) / valid;
       const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
       if (r == 32)
-        k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
+        k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
       else if (r == 24)
-        k_heat_warp<24><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
+        k_heat_warp<24><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
       else
-        k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k);
+        k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
     } else {
       const int r = heat_cells_per_thread();
       const uint64_t valid = (uint64_t)kRegThreads * r - 2 * (uint64_t)k;

@@ -1,0 +1,48 @@
+"""Small instances of every builtin/bound kernel and one NVRTC kernel, for
+compute-sanitizer (scripts/sanitize.sh).  Results are checked by tests/ -m
+gpu; here only the memory/race/sync behaviour matters."""
+import numpy as np
+
+from paper_1810_11482_b200 import Runtime
+from paper_1810_11482_b200.bindings import kernel_source
+
+with Runtime(devices=[0]) as rt:
+    d = rt.get_all_devices().get()[0]
+    rng = np.random.default_rng(3)
+    n = 100_001
+    X, Y = d.create_buffer(n * 8).get(), d.create_buffer(n * 8).get()
+    X.enqueue_write(0, rng.random(n))
+    bp = d.create_builtin_program().get()
+    for name in ("heat", "dot_f32", "mandelbrot_rows"):
+        bp.build(name).get()
+    g = ((n + 255) // 256, 1, 1), (256, 1, 1)
+    bp.run([X, Y, n, 130], "heat", *g).get()          # fused path
+    X.enqueue_write(0, rng.standard_normal(n))
+    bp.run([X, Y, n, 65], "heat", *g).get()           # unfused path + split pass
+    for op in ("copy", "scale", "add", "triad"):
+        p = d.create_program_with_source(kernel_source("stream")).get()
+        p.build(op).get()
+        args = {"copy": [Y, X, n], "scale": [Y, X, 2.0, n], "add": [Y, X, X, n],
+                "triad": [Y, X, X, 3.0, n]}[op]
+        p.run(args, op, *g).get()
+    F1 = d.create_buffer(n * 4).get()
+    F1.enqueue_write(0, rng.random(n, dtype=np.float32))
+    O = d.create_buffer(8).get()
+    bp.run([F1, F1, O, n], "dot_f32", *g).get()
+    M = d.create_buffer(97 * 61 * 4).get()
+    bp.run([M, 97, 61, -2.0, 1.0, -1.5, 1.5, 4.0, 300, 1, 3], "mandelbrot_rows", *g).get()
+    pp = d.create_program_with_source(kernel_source("partition")).get()
+    pp.build("partition").get()
+    pp.run([X, 7, n], "partition", *g).get()
+    U = d.create_buffer(n * 4).get()
+    U.enqueue_write(0, rng.integers(0, 2**32, n, dtype=np.uint32))
+    R = d.create_buffer(4).get()
+    sp = d.create_program_with_source(kernel_source("sum")).get()
+    sp.build("sum").get()
+    sp.run([U, R, n], "sum", (1, 1, 1), (32, 1, 1)).get()
+    # an unbound kernel: NVRTC path
+    src = ("kernel inc(a : buffer_u32, n : scalar_u32) { if (gtid < n) { a[gtid] = a[gtid] + u32(1); } }")
+    jp = d.create_program_with_source(src).get()
+    jp.build("inc").get()
+    jp.run([U, n], "inc", *g).get()
+    print("workloads ok")
