@@ -20,6 +20,8 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kMaxBlocks = 148 * 4;
+constexpr int kSumCtasPerSm = 3;
+constexpr int kDotCtasPerSm = 2;
 
 // Lives at kScratchOffset of the per-stream scratch (the Mandelbrot work
 // queue uses offset 32768); `partial` has one slot per CTA of the launch.
@@ -148,14 +150,21 @@ __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ 
   if (fold<double>(sc, acc, &total)) res[0] = total;
 }
 
-// Grid: persistent, 4 CTAs (2048 threads, full occupancy) per SM with a
-// grid-stride loop. A one-shot grid (one unrolled round per thread) measured
-// slower on B200 — 0.198 vs 0.167 ms for sum 2^28, 3.46 vs 2.60 ms for dot
-// 2^31 (profiles/r01_reduce_grid.txt): the per-CTA atomic ticket and the
-// last CTA's fold over ~10^5 partials cost more than the tail it balances.
-int grid_for(ofl_stream* s, uint64_t vec_units, int unroll) {
+// Grid: persistent, `cps` CTAs of 512 threads per SM with a grid-stride
+// loop.  A one-shot grid (one unrolled round per thread) measured slower on
+// B200 — 0.198 vs 0.167 ms for sum 2^28, 3.46 vs 2.60 ms for dot 2^31
+// (profiles/r01_reduce_grid.txt): the per-CTA atomic ticket and the last
+// CTA's fold over ~10^5 partials cost more than the tail it balances.  CTAs
+// per SM per kernel from the read-bandwidth sweep (scripts/probes/
+// read_bw_probe.cu, scripts/reduce_sweep.sh); OFL_REDUCE_CPS overrides.
+int grid_for(ofl_stream* s, uint64_t vec_units, int unroll, int cps) {
+  static const int env_cps = [] {
+    const char* e = getenv("OFL_REDUCE_CPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_cps >= 1 && env_cps <= 4) cps = env_cps;
   uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
-  uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * 4;
+  uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * cps;
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
@@ -175,7 +184,7 @@ extern "C" int ofl_sum_u32(ofl_stream* s, const uint32_t* in, uint32_t* res, uin
     return ofl::set_error(OFL_ERR_BAD_ARGS, "sum input must be 16-byte aligned");
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
-  const int blocks = grid_for(s, n >> 2, 4);
+  const int blocks = grid_for(s, n >> 2, 4, kSumCtasPerSm);
   void* scratch = nullptr;
   int st = ofl::stream_scratch(s, scratch_bytes(blocks), &scratch);
   if (st) return st;
@@ -193,7 +202,7 @@ extern "C" int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double
     return ofl::set_error(OFL_ERR_BAD_ARGS, "dot operands must be 16-byte aligned");
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
-  const int blocks = grid_for(s, n >> 2, 2);
+  const int blocks = grid_for(s, n >> 2, 2, kDotCtasPerSm);
   void* scratch = nullptr;
   int st = ofl::stream_scratch(s, scratch_bytes(blocks), &scratch);
   if (st) return st;
