@@ -410,19 +410,21 @@ def run_ours(args) -> None:
     # alternate between two streams and two device buffer sets (Alg. 1
     # style) so step k's read overlaps step k+1's writes on the full-duplex
     # link; every step's copies are inside the timed region.
-    sets = [(A, B, C, 0), tuple(dev.create_buffer(n * 8).get() for _ in range(3)) + (dev.create_stream(),)]
-    outs = [a_host, pinned_empty(n * 8, np.float64)]
+    nsets = max(2, args.e2e_sets)
+    sets = [(A, B, C, 0)] + [tuple(dev.create_buffer(n * 8).get() for _ in range(3))
+                             + (dev.create_stream(),) for _ in range(nsets - 1)]
+    outs = [a_host] + [pinned_empty(n * 8, np.float64) for _ in range(nsets - 1)]
 
     def e2e(steps: int) -> None:
         pending = []
         for k in range(steps):
-            Ak, Bk, Ck, sk = sets[k & 1]
-            if len(pending) == 2:
+            Ak, Bk, Ck, sk = sets[k % nsets]
+            if len(pending) == nsets:
                 pending.pop(0).get()
             Bk.enqueue_write(0, b_host, sk)
             Ck.enqueue_write(0, c_host, sk)
             prog.run([Ak, Bk, Ck, s, n], "triad", grid, block, sk)
-            pending.append(Ak.enqueue_read_into(0, outs[k & 1], sk))
+            pending.append(Ak.enqueue_read_into(0, outs[k % nsets], sk))
         for t in pending:
             t.get()
 
@@ -487,7 +489,7 @@ def run_ours(args) -> None:
                 "steps": args.e2e_steps,
                 "ms_per_step": round(e2e_s / args.e2e_steps * 1e3, 3),
                 "schedule": "write b, write c (pinned), run, read_into a (pinned) per step; "
-                "steps alternate over 2 streams x 2 device buffer sets; wall clock",
+                f"steps rotate over {nsets} streams x {nsets} device buffer sets; wall clock",
             },
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
@@ -509,6 +511,8 @@ def main(argv=None) -> None:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--n", type=int, default=1 << 25)
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-sets", type=int, default=2,
+                    help="device buffer sets / streams the e2e steps rotate over")
     ap.add_argument("--overhead-steps", type=int, default=10000)
     ap.add_argument("--no-overhead", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
