@@ -150,6 +150,19 @@ int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t 
  * Temporal blocking: `tb` steps are fused per pass through HBM (1 = none). */
 int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, int tb,
              uint64_t* ticket);
+/* One slab pass of the multi-GPU heat equation (BASELINE config 2; the
+ * reference has no multi-device stencil — harness.py:199-230 is single-device,
+ * its cross-device path is copy() through the host, handles.py:119-145):
+ * k (1..64) stencil.k steps of slab x -> y (length n, local cells 0 and n-1
+ * held fixed), writing y only for the owned cells [own_lo, own_hi), and the
+ * first / last h owned cells also straight into left_ghost[0..h) /
+ * right_ghost[0..h) — the neighbouring slabs' ghost cells, on devices
+ * left_dev / right_dev (peer stores over NVLink from the kernel; either
+ * pointer may be NULL).  The caller orders each pass after the neighbours'
+ * previous pass (ofl_stream_wait). */
+int ofl_heat_slab(ofl_stream* s, const double* x, double* y, uint64_t n, int k, uint64_t own_lo,
+                  uint64_t own_hi, double* left_ghost, int left_dev, double* right_ghost,
+                  int right_dev, uint64_t h, uint64_t* ticket);
 
 /* mandelbrot.k (bench/kernels/mandelbrot.k:6-29), pixels gtid in
  * [0, min(width*height mod 2^32, items)); counts written at out[gtid].

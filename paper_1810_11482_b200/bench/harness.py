@@ -402,14 +402,23 @@ class HeatSlabs:
     """1-D slab decomposition of the heat equation over several devices.
 
     Device g owns cells [lo_g, hi_g) and keeps `halo` ghost cells on each
-    inner side.  Every `halo` steps it advances its slab with the temporal-
-    blocking heat builtin (the ghosts absorb the shrinking valid region),
-    then the owned boundary strips are copied into the neighbours' ghosts —
-    device-side copies ordered on the default streams of both ends, no host
-    round trip.  Global endpoints stay fixed because a slab's outer end is
-    either the true endpoint or a ghost that is overwritten before use."""
+    inner side.  Every `halo` steps it advances its slab by one temporal-
+    blocked pass (the ghosts absorb the shrinking valid region) and the
+    owned boundary strips must reach the neighbours' ghosts.  Global
+    endpoints stay fixed because a slab's outer end is either the true
+    endpoint or a ghost that is overwritten before use.
 
-    def __init__(self, devices: Sequence[DeviceHandle], x: np.ndarray, halo: int = 1):
+    Exchange (``fused``, default when halo <= 64 and all devices are in this
+    process): the pass kernel itself stores its first / last `halo` owned
+    cells into the neighbours' ghost cells through peer pointers (NVLink
+    stores, ``ofl_heat_slab``), and each device's next pass waits on its two
+    neighbours' previous pass (cross-device events) — no copy operations and
+    no host round trip.  ``fused=False``: the pass runs through the public
+    ``heat`` builtin and the strips move by device-side ``copy()``
+    (``cudaMemcpyPeerAsync``) on the default streams of both ends."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], x: np.ndarray, halo: int = 1,
+                 fused: Optional[bool] = None):
         G = len(devices)
         n = x.size
         if halo < 1:
@@ -433,13 +442,18 @@ class HeatSlabs:
             A.enqueue_write(0, local.tobytes())
             self.a.append(A)
             self.b.append(B)
-        self.progs = [_builtin(d, "heat") for d in self.devices]
+        self.fused = (halo <= 64) if fused is None else bool(fused)
+        if self.fused and halo > 64:
+            raise BadArgsError("the fused exchange needs halo <= 64 (one pass per exchange)")
+        self.progs = None if self.fused else [_builtin(d, "heat") for d in self.devices]
 
     def _exchange(self, cur: list) -> list:
         return [copy(cur[sg], s_cell * 8, cur[dg], d_cell * 8, cells * 8)
                 for sg, s_cell, dg, d_cell, cells in decomp.halo_exchanges(self.layout, self.halo)]
 
     def run(self, steps: int):
+        if self.fused:
+            return self._run_fused(steps)
         cur, nxt = self.a, self.b
         left = steps
         toks = []
@@ -456,6 +470,44 @@ class HeatSlabs:
         self.a, self.b = cur, nxt
         return when_all(toks) if toks else None
 
+    def _run_fused(self, steps: int):
+        import ctypes
+
+        from .. import _native
+
+        objs = lambda hs: [h._runtime.local._buffer(h.gid) for h in hs]  # noqa: E731
+        cur_h, nxt_h = self.a, self.b
+        cur, nxt = objs(cur_h), objs(nxt_h)
+        G, lay, h = len(self.devices), self.layout, self.halo
+        streams = [o.device.stream(0) for o in cur]
+        ords = [o.device.ordinal for o in cur]
+        lib = streams[0].lib
+        prev = [0] * G
+        ticket = ctypes.c_uint64()
+        left = steps
+        while left > 0:
+            k = min(h, left)
+            now = []
+            for g in range(G):
+                st = streams[g]
+                for nb in (g - 1, g + 1):
+                    if 0 <= nb < G and prev[nb]:
+                        _native.check(lib.ofl_stream_wait(st.ptr, streams[nb].ptr, prev[nb]),
+                                      "halo ordering")
+                own_lo = lay[g].left
+                lghost = (nxt[g - 1].ptr + (lay[g - 1].left + lay[g - 1].owned) * 8) if g else None
+                rghost = nxt[g + 1].ptr if g + 1 < G else None
+                _native.check(lib.ofl_heat_slab(
+                    st.ptr, cur[g].ptr, nxt[g].ptr, lay[g].length, k, own_lo, own_lo + lay[g].owned,
+                    lghost, ords[g - 1] if g else -1, rghost, ords[g + 1] if g + 1 < G else -1, h,
+                    ctypes.byref(ticket)), "heat slab pass")
+                now.append(ticket.value)
+            prev = now
+            cur, nxt, cur_h, nxt_h = nxt, cur, nxt_h, cur_h
+            left -= k
+        self.a, self.b = cur_h, nxt_h
+        return when_all([streams[g].token(prev[g]) for g in range(G)]) if steps else None
+
     def gather(self) -> np.ndarray:
         out = np.empty(self.n)
         reads = []
@@ -467,8 +519,9 @@ class HeatSlabs:
         return out
 
 
-def heat_multi(devices: Sequence[DeviceHandle], x: np.ndarray, steps: int, halo: int = 1) -> np.ndarray:
-    slabs = HeatSlabs(devices, np.asarray(x, dtype=np.float64), halo)
+def heat_multi(devices: Sequence[DeviceHandle], x: np.ndarray, steps: int, halo: int = 1,
+               fused: Optional[bool] = None) -> np.ndarray:
+    slabs = HeatSlabs(devices, np.asarray(x, dtype=np.float64), halo, fused)
     slabs.run(steps)
     return slabs.gather()
 

@@ -280,10 +280,21 @@ __device__ __forceinline__ bool warp_tile_steps(double (&a)[R], double (&b)[R], 
               : warp_steps<R, false, false>(a, b, lane, g0, nn, tb);
 }
 
-template <int R>
+// Where a slab pass (ofl_heat_slab) puts its results: only the owned cells
+// [own_lo, own_hi) of y, plus the first / last h owned cells straight into
+// the neighbouring slabs' ghost cells (left / right, usually on peer GPUs:
+// the stores travel over NVLink from this kernel, no separate copy).
+struct SlabOut {
+  int64_t own_lo, own_hi, h;
+  double* left;   // receives y[own_lo, own_lo + h), or null
+  double* right;  // receives y[own_hi - h, own_hi), or null
+};
+
+template <int R, bool kSlab = false>
 __global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __restrict__ x,
                                                             double* __restrict__ y, uint64_t n,
-                                                            int tb, bool fma_ok) {
+                                                            int tb, bool fma_ok,
+                                                            SlabOut so = SlabOut{}) {
   constexpr int kCells = 32 * R;
   const int lane = threadIdx.x & 31;
   const int64_t wtile = (int64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
@@ -303,7 +314,16 @@ __global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __rest
   for (int i = 0; i < R; ++i) {
     const int local = lane * R + i;
     const int64_t g = g0 + i;
-    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = odd ? b[i] : a[i];
+    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) {
+      const double v = odd ? b[i] : a[i];
+      if (!kSlab) {
+        y[g] = v;
+      } else if (g >= so.own_lo && g < so.own_hi) {
+        y[g] = v;
+        if (so.left && g < so.own_lo + so.h) so.left[g - so.own_lo] = v;
+        if (so.right && g >= so.own_hi - so.h) so.right[g - (so.own_hi - so.h)] = v;
+      }
+    }
   }
 }
 
@@ -535,5 +555,30 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
     left -= (uint64_t)k;
   }
   ofl::count_launch(launches);
+  return q.finish(ticket);
+}
+
+extern "C" int ofl_heat_slab(ofl_stream* s, const double* x, double* y, uint64_t n, int k,
+                             uint64_t own_lo, uint64_t own_hi, double* left_ghost, int left_dev,
+                             double* right_ghost, int right_dev, uint64_t h, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (n < 1 || k < 1 || k > 64)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab needs n >= 1 and 1 <= k <= 64");
+  if (own_lo > own_hi || own_hi > n || h > own_hi - own_lo)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: bad owned range / halo");
+  if (x == y) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: x and y must differ");
+  if (left_ghost && left_dev != s->dev) ofl::enable_peer(s->dev, left_dev);
+  if (right_ghost && right_dev != s->dev) ofl::enable_peer(s->dev, right_dev);
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  SlabOut so{(int64_t)own_lo, (int64_t)own_hi, (int64_t)h, h ? left_ghost : nullptr,
+             h ? right_ghost : nullptr};
+  const uint64_t valid = 32ull * 24 - 2 * (uint64_t)k;
+  const uint64_t warps = (n + valid - 1) / valid;
+  const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
+  k_heat_warp<24, true><<<blocks, kWarpThreads, 0, s->cs>>>(x, y, n, k, heat_fused(), so);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return ofl::cuda_error(e, "heat slab launch");
+  ofl::count_launch();
   return q.finish(ticket);
 }

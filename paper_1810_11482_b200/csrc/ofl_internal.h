@@ -50,6 +50,8 @@ int cuda_error(cudaError_t e, const char* what);
 cudaError_t use_device(int dev);
 int num_sms(int dev);
 void count_launch(uint64_t n = 1);
+// cudaDeviceEnablePeerAccess(from -> to) once per pair, if the pair supports it
+void enable_peer(int from, int to);
 // Scratch of at least `bytes` on the stream's device (caller holds s->mu).
 int stream_scratch(ofl_stream* s, size_t bytes, void** out);
 

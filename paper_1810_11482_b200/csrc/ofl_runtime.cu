@@ -177,6 +177,27 @@ static void CUDART_CB host_complete(void* p) {
 static std::mutex g_zero_mu[kMaxDev];
 static cudaStream_t g_zero_stream[kMaxDev];
 
+// Direct peer access for copies and kernel peer stores (once per pair).
+static std::mutex g_peer_mu;
+static bool g_peer_done[kMaxDev][kMaxDev];
+
+void enable_peer(int from, int to) {
+  if (from == to || from < 0 || to < 0 || from >= kMaxDev || to >= kMaxDev) return;
+  std::lock_guard<std::mutex> g(g_peer_mu);
+  if (g_peer_done[from][to]) return;
+  g_peer_done[from][to] = true;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, from, to) == cudaSuccess && can) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(from);
+    cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+  (void)cudaGetLastError();
+}
+
 }  // namespace ofl
 
 using namespace ofl;
@@ -338,26 +359,6 @@ int ofl_d2h(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t*
 }
 int ofl_d2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket) {
   return copy_op(s, dst, src, bytes, cudaMemcpyDeviceToDevice, ticket);
-}
-
-static std::mutex g_peer_mu;
-static bool g_peer_done[kMaxDev][kMaxDev];
-
-static void enable_peer(int from, int to) {
-  if (from == to || from < 0 || to < 0 || from >= kMaxDev || to >= kMaxDev) return;
-  std::lock_guard<std::mutex> g(g_peer_mu);
-  if (g_peer_done[from][to]) return;
-  g_peer_done[from][to] = true;
-  int can = 0;
-  if (cudaDeviceCanAccessPeer(&can, from, to) == cudaSuccess && can) {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    cudaSetDevice(from);
-    cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
-    if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
-    if (cur >= 0) cudaSetDevice(cur);
-  }
-  (void)cudaGetLastError();
 }
 
 int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev, uint64_t bytes,

@@ -63,16 +63,52 @@ def test_adversarial_ranges_never_corrupt(offset, size, blob):
         assert offset + size > 128
 
 
-@pytest.mark.parametrize("halo,steps", [(64, 200), (16, 50), (7, 22)])
-def test_heat_multi_device_temporal_halo(rt2, halo, steps):
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("halo,steps", [(64, 200), (16, 50), (7, 22), (1, 9)])
+def test_heat_multi_device_temporal_halo(rt2, halo, steps, fused):
     from paper_1810_11482_b200.bench.harness import heat_multi
 
     import oracle
 
     devices = rt2.get_all_devices().get()
     x = np.random.default_rng(halo).random(200_003)
-    got = heat_multi(devices, x, steps, halo=halo)
+    got = heat_multi(devices, x, steps, halo=halo, fused=fused)
     assert got.tobytes() == oracle.heat(x, steps, threads=0).tobytes()
+
+
+@pytest.mark.parametrize("parts,halo,steps", [(4, 64, 301), (5, 3, 40), (3, 64, 64)])
+def test_heat_fused_exchange_many_slabs(parts, halo, steps):
+    """Peer-store halo exchange between several slabs (logical devices on
+    GPU 0, each with its own streams, so passes really run concurrently and
+    the cross-device ordering is exercised), on data that sends some warps
+    down the unfused update path."""
+    from paper_1810_11482_b200 import Runtime
+    from paper_1810_11482_b200.bench.harness import heat_multi
+
+    import oracle
+
+    x = np.random.default_rng(parts).random(50_000 * parts + 17)
+    x[1000:2500] = np.random.default_rng(1).standard_normal(1500)
+    with Runtime(devices=[0] * parts) as rt:
+        devices = rt.get_all_devices().get()
+        got = heat_multi(devices, x, steps, halo=halo, fused=True)
+    exp = oracle.heat(x, steps, threads=0)
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+
+
+def test_heat_fused_exchange_real_peers():
+    """Two physical GPUs when the box has them (NVLink peer stores)."""
+    from paper_1810_11482_b200 import Runtime, _native
+    from paper_1810_11482_b200.bench.harness import heat_multi
+
+    import oracle
+
+    if _native.device_count() < 2:
+        pytest.skip("one GPU on this box: peer stores exercised on logical devices only")
+    x = np.random.default_rng(5).random(1_000_003)
+    with Runtime(devices=[0, 1]) as rt:
+        got = heat_multi(rt.get_all_devices().get(), x, 200, halo=64, fused=True)
+    assert got.tobytes() == oracle.heat(x, 200, threads=0).tobytes()
 
 
 def test_dot_two_logical_devices_host_sum(rt2):
