@@ -23,7 +23,9 @@ from __future__ import annotations
 import ctypes
 import itertools
 import os
+import select
 import threading
+import time
 from typing import Any, Callable, Optional
 
 from . import _native
@@ -37,6 +39,24 @@ _thread: Optional[threading.Thread] = None
 _thread_lock = threading.Lock()
 
 
+# With nothing completing for this long, the completion thread checks the
+# streams of the tokens it waits for: a sticky device fault stops the CUDA
+# host-function callbacks, so without this a then() on a faulted stream
+# would never fire.  Idle-time only — busy streams are never polled.
+WATCHDOG_S = 1.0
+
+
+def _watchdog() -> None:
+    with _pending_lock:
+        items = list(_pending.items())
+    for tid, tok in items:
+        if tok._state == _PENDING:
+            tok._poll()  # ofl_query: a fault fails the token (and its continuations)
+        if tok._state != _PENDING:
+            with _pending_lock:
+                _pending.pop(tid, None)
+
+
 def _completion_loop(fd: int) -> None:
     lib = _native.load()
     cap = 1024
@@ -44,6 +64,11 @@ def _completion_loop(fd: int) -> None:
     count = ctypes.c_int(0)
     while True:
         try:
+            ready, _, _ = select.select([fd], [], [], WATCHDOG_S)
+            if not ready:
+                if _pending:
+                    _watchdog()
+                continue
             os.read(fd, 8)
         except InterruptedError:
             continue
@@ -143,7 +168,18 @@ class DeviceToken(CompletionToken):
         if self._state != _PENDING:
             return True
         if timeout is not None:
-            return super()._block(timeout)
+            # wait for the completion callback in slices, querying the stream
+            # in between so that a device fault (which stops callbacks)
+            # surfaces as an error instead of a timeout
+            event = threading.Event()
+            self._on_done(lambda _t: event.set())
+            deadline = time.monotonic() + timeout
+            while True:
+                left = deadline - time.monotonic()
+                if event.wait(min(0.05, max(left, 0.0))) or self._poll():
+                    return True
+                if left <= 0:
+                    return False
         s = self._stream
         status = s.lib.ofl_wait(s.ptr, self._ticket)
         if status:

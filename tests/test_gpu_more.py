@@ -4,6 +4,7 @@ with a temporal-blocking halo, dot over two logical devices."""
 
 from __future__ import annotations
 
+import os
 import numpy as np
 import pytest
 from hypothesis import given, settings
@@ -122,3 +123,65 @@ def test_dot_two_logical_devices_host_sum(rt2):
     got = dot_multi(devices, a, b)  # no NCCL across logical devices of one GPU
     exp = oracle.dot_f32(a, b)
     assert abs(got - exp) <= 1e-12 * abs(exp)
+
+
+FAULT_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+from paper_1810_11482_b200 import Runtime, InternalError, when_all
+from paper_1810_11482_b200.bindings import kernel_source
+
+rt = Runtime(devices=[0])
+dev = rt.get_all_devices().get()[0]
+n = 1 << 20
+A, B, C = (dev.create_buffer(n * 8).get() for _ in range(3))
+p = dev.create_program_with_source(kernel_source("stream")).get()
+p.build("triad").get()
+p.run([A, B, C, 3.0, n], "triad", (n // 256, 1, 1), (256, 1, 1)).get()   # healthy
+# corrupt the device pointer behind A (test-only): the kernel faults on the GPU
+obj = rt.local._buffer(A.gid)
+good = obj.ptr
+obj.ptr = 0x10
+bad = p.run([A, B, C, 3.0, n], "triad", (n // 256, 1, 1), (256, 1, 1))
+after = B.enqueue_read(0, 8)           # queued behind the faulting kernel
+chain = when_all([bad, after])
+cont = bad.then(lambda v: "ran")       # armed before the fault lands
+seen = []
+for name, tok in (("then", cont), ("kernel", bad), ("read", after), ("when_all", chain)):
+    try:
+        tok.get(timeout=60)
+        seen.append(name + ":ok")
+    except InternalError as exc:
+        seen.append(name + ":InternalError")
+    except TimeoutError:
+        seen.append(name + ":timeout")
+# the context is poisoned (sticky error): new work fails instead of hanging
+try:
+    p.run([B, B, C, 3.0, n], "triad", (n // 256, 1, 1), (256, 1, 1)).get(timeout=60)
+    seen.append("new:ok")
+except InternalError:
+    seen.append("new:InternalError")
+except TimeoutError:
+    seen.append("new:timeout")
+obj.ptr = good
+print(" ".join(seen), flush=True)
+import os
+os._exit(0)
+"""
+
+
+def test_device_fault_fails_tokens_not_hangs():
+    """A kernel fault (sticky CUDA error) comes back as InternalError on the
+    faulting op, on ops queued behind it and on their when_all, and later
+    ops fail fast (SURVEY §5 failure detection).  Runs in a subprocess: the
+    CUDA context is unusable afterwards."""
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", FAULT_SCRIPT, repo], capture_output=True,
+                       text=True, timeout=300)
+    line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
+    assert line == ("then:InternalError kernel:InternalError read:InternalError "
+                    "when_all:InternalError new:InternalError"), line
