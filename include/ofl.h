@@ -145,6 +145,14 @@ int ofl_stream_op(ofl_stream* s, int op, double* a, const double* b, const doubl
  *   y[i] = x[i] at i==0 or i==n-1, else 0.5*x[i-1] + x[i] + 0.5*x[i+1]   */
 int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t items,
                 uint64_t* ticket);
+/* stencil2d.k (paper_1810_11482_b200/kernels/stencil2d.k — the 2-D form
+ * of bench/kernels/stencil.k, in the reference's kernel language): for
+ * gtid < min(items, (w*h) mod 2^32), row = gtid / w, col = gtid % w:
+ *   y[g] = x[g] on the boundary ring, else 0.25*(((x[g-w]+x[g-1])+x[g+1])+x[g+w]).
+ * x_elems bounds the loads (cells past it are never executed by a checked
+ * launch; see bindings._stencil2d_oob). */
+int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t w, uint32_t h,
+                  uint64_t items, uint64_t x_elems, uint64_t* ticket);
 /* `steps` applications of stencil.k ping-ponging x <-> y (heat equation,
  * BASELINE config 2); the final state is in x if steps is even else in y.
  * Temporal blocking: `tb` steps are fused per pass through HBM (1 = none). */

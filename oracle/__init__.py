@@ -53,6 +53,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_stream.restype = None
         L.oracle_stencil.argtypes = [vp, vp, u64, u64, i32]
         L.oracle_stencil.restype = None
+        L.oracle_stencil2d.argtypes = [vp, vp, u32, u32, u64, i32]
+        L.oracle_stencil2d.restype = None
         L.oracle_heat.argtypes = [vp, vp, u64, u64, i32]
         L.oracle_heat.restype = None
         L.oracle_mandelbrot.argtypes = [vp, u32, u32, f64, f64, f64, f64, f64, u32, u64, u32, u32, i32]
@@ -98,6 +100,26 @@ def stencil(x: np.ndarray, items=None, out=None, threads: int = 1) -> np.ndarray
     y = np.zeros_like(x) if out is None else out
     lib().oracle_stencil(_p(x), _p(y), n, n if items is None else items, threads)
     return y
+
+
+def stencil2d(x: np.ndarray, w: int, h: int, items=None, out=None, threads: int = 1) -> np.ndarray:
+    """One stencil2d.k step over a row-major w x h grid; items beyond
+    min((w*h) mod 2^32, items) keep `out`'s content."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x) if out is None else out
+    cells = (w * h) & 0xFFFFFFFF
+    lib().oracle_stencil2d(_p(x), _p(y), w, h, cells if items is None else items, threads)
+    return y
+
+
+def heat2d(x: np.ndarray, w: int, h: int, steps: int, threads: int = 1) -> np.ndarray:
+    """`steps` stencil2d.k applications ping-ponging; returns the final state."""
+    a = np.array(x, dtype=np.float64, copy=True)
+    b = a.copy()
+    for _ in range(steps):
+        stencil2d(a, w, h, out=b, threads=threads)
+        a, b = b, a
+    return a
 
 
 def heat(x: np.ndarray, steps: int, threads: int = 1) -> np.ndarray:

@@ -23,6 +23,15 @@ def stencil(x: np.ndarray) -> np.ndarray:
     return y
 
 
+def stencil2d(x: np.ndarray, w: int, h: int) -> np.ndarray:
+    """kernels/stencil2d.k restated over the whole grid (w, h >= 1)."""
+    X = np.asarray(x, dtype=np.float64).reshape(h, w)
+    Y = X.copy()
+    if h > 2 and w > 2:
+        Y[1:-1, 1:-1] = 0.25 * (((X[:-2, 1:-1] + X[1:-1, :-2]) + X[1:-1, 2:]) + X[2:, 1:-1])
+    return Y.ravel()
+
+
 def stencil_seq(x) -> list:
     """tests/oracles.py:13-20 restated."""
     out = list(x)

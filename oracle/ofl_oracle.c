@@ -141,6 +141,44 @@ void oracle_heat(double* x, double* y, uint64_t n, uint64_t steps, int threads) 
   }
 }
 
+/* stencil2d.k (paper_1810_11482_b200/kernels/stencil2d.k; the reference
+ * language, executed as the reference executor does, kernel/codegen.py:
+ * 107-128): items gtid < min((w*h) mod 2^32, items), u32 row/col, boundary
+ * ring held, interior 0.25 * (((N + W) + E) + S) left to right. */
+struct stencil2d_ctx {
+  const double* x;
+  double* y;
+  uint32_t w, h;
+};
+
+static void stencil2d_range(int64_t lo, int64_t hi, void* p) {
+  struct stencil2d_ctx* k = (struct stencil2d_ctx*)p;
+  const double* x = k->x;
+  double* y = k->y;
+  const uint32_t w = k->w, h = k->h;
+  for (int64_t i = lo; i < hi; ++i) {
+    const uint32_t g = (uint32_t)i;
+    const uint32_t row = g / w;
+    const uint32_t col = g - row * w;
+    if (row == 0 || row == h - 1u || col == 0 || col == w - 1u) {
+      y[g] = x[g];
+    } else {
+      double t = x[g - w] + x[g - 1];
+      t = t + x[g + 1];
+      t = t + x[g + w];
+      y[g] = 0.25 * t;
+    }
+  }
+}
+
+void oracle_stencil2d(const double* x, double* y, uint32_t w, uint32_t h, uint64_t items,
+                      int threads) {
+  const uint64_t cells = (uint64_t)(uint32_t)(w * h);
+  const uint64_t m = items < cells ? items : cells;
+  struct stencil2d_ctx k = {x, y, w, h};
+  parallel_for((int64_t)m, threads, stencil2d_range, &k);
+}
+
 /* mandelbrot.k (bench/kernels/mandelbrot.k:6-29); validator harness.py:133-158,
  * tests/oracles.py:30-55.  Pixels gtid < min((w*h) mod 2^32, items), rows
  * py = row_first + k*row_step only. */

@@ -121,6 +121,73 @@ def _stencil_launch(st, v, items, ticket):
     return st.lib.ofl_stencil(st.ptr, x.ptr, y.ptr, n, m, ticket)
 
 
+# -- stencil2d -------------------------------------------------------------------
+
+
+def _stencil2d_oob(v, items):
+    """First out-of-range access in the reference executor's order: items run
+    in gtid order; per item the store index is checked, then the loads left
+    to right (boundary: u[g]; interior: u[g-w], u[g-1], u[g+1], u[g+w])."""
+    x, y, w, h = v
+    cells = (w * h) & M32
+    m = min(cells, items)
+    if m == 0:
+        return None
+    lx, ly = x.elements("buffer_f64"), y.elements("buffer_f64")
+    if lx >= cells and ly >= cells:
+        return None
+
+    def boundary(g):
+        row, col = divmod(g, w)
+        return row == 0 or row == h - 1 or col == 0 or col == w - 1
+
+    def first_interior_from(g):
+        g = max(g, 0)
+        row, col = divmod(g, w)
+        if row == 0:
+            row, col = 1, 1
+        elif col == 0:
+            col = 1
+        elif col == w - 1:
+            row, col = row + 1, 1
+        if row >= h - 1 or col >= w - 1:
+            return None
+        return row * w + col
+
+    def first_boundary_from(g):
+        return g if boundary(g) else (g // w) * w + w - 1
+
+    cand = [ly, first_boundary_from(lx) if lx < m else None,
+            first_interior_from(lx - w), first_interior_from(lx - 1),
+            first_interior_from(lx + 1), first_interior_from(lx)]
+
+    def failing(g):
+        if g >= m:
+            return None
+        if g >= ly:
+            return g
+        loads = (g,) if boundary(g) else (g - w, g - 1, g + 1, g + w)
+        for idx in loads:
+            if idx >= lx:
+                return idx
+        return None
+
+    return _first_oob(cand, failing)
+
+
+def _stencil2d_launch(st, v, items, ticket):
+    x, y, w, h = v
+    cells = (w * h) & M32
+    m = min(cells, items)
+    if m and x is y:
+        raise BadArgsError(
+            "stencil2d: in-place update (u is u_next) is order-dependent; use two buffers"
+        )
+    if w * h >= 1 << 32:
+        raise BadArgsError("stencil2d: grids of 2^32 cells or more are not supported")
+    return st.lib.ofl_stencil2d(st.ptr, x.ptr, y.ptr, w, h, m, x.elements("buffer_f64"), ticket)
+
+
 # -- mandelbrot ------------------------------------------------------------------
 
 
@@ -271,8 +338,8 @@ def _source(name: str) -> str:
 
 
 def kernel_source(name: str) -> str:
-    """Source text of a bundled kernel program (stream, stencil, mandelbrot,
-    sum, partition)."""
+    """Source text of a bundled kernel program (stream, stencil, stencil2d,
+    mandelbrot, sum, partition)."""
     return _source(name)
 
 
@@ -284,6 +351,8 @@ def _table() -> dict:
         ("stream", "add"): lambda k: _stream_binding("add", _native.STREAM_ADD, k),
         ("stream", "triad"): lambda k: _stream_binding("triad", _native.STREAM_TRIAD, k),
         ("stencil", "stencil"): lambda k: Binding("stencil", k, _stencil_launch, _stencil_oob),
+        ("stencil2d", "stencil2d"): lambda k: Binding("stencil2d", k, _stencil2d_launch,
+                                                      _stencil2d_oob),
         ("mandelbrot", "mandelbrot"): lambda k: Binding("mandelbrot", k, _mandel_launch, _mandel_oob),
         ("sum", "sum"): lambda k: Binding("sum", k, _sum_launch, _sum_oob),
         ("partition", "partition"): lambda k: Binding(

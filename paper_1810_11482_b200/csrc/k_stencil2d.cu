@@ -1,0 +1,221 @@
+// 2-D 5-point Jacobi step (paper_1810_11482_b200/kernels/stencil2d.k; the
+// reference has only the 1-D stencil.k — this is the same language run by
+// the same executor rules, kernel/codegen.py:107-128):
+//
+//   cells = (w*h) mod 2^32; for gtid < min(items, cells), row = gtid / w,
+//   col = gtid - row*w (u32):
+//     boundary ring (row 0 / h-1, col 0 / w-1):  y[g] = x[g]
+//     interior: y[g] = 0.25 * (((x[g-w] + x[g-1]) + x[g+1]) + x[g+w])
+//
+// evaluated left to right, round-to-nearest, no contraction: bit-exact.
+//
+// HBM-bound (16 B per cell: one read, one write).  k_stencil2d_march: a warp
+// owns a 64-column x R-row strip; each lane holds two adjacent columns as one
+// double2 and marches down the rows keeping (up, cur, down) in registers, so
+// every cell is loaded from HBM once (+2/R for the strip's halo rows); the
+// west/east neighbours come from the adjacent lanes by shuffle, the two
+// outside the strip from a scalar load by lanes 0 / 31 (L2 hits: the
+// neighbouring strips load them too).  Stores are 128-bit, streaming.
+// k_stencil2d_cells: one thread per cell with u32 index arithmetic exactly
+// as the .k text — odd widths (unaligned rows), grids whose w*h wraps 2^32,
+// unaligned buffers.
+#include <cstdlib>
+
+#include "ofl_internal.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRows = 32;  // rows per warp strip
+
+__device__ __forceinline__ double interior(double n, double w, double e, double s) {
+  return __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(n, w), e), s));
+}
+
+__device__ __forceinline__ double2 ld2(const double* x, uint64_t idx, uint64_t lx) {
+  // idx is even (16-byte aligned pair); either half may lie past the buffer
+  if (idx + 1 < lx) return __ldcs(reinterpret_cast<const double2*>(x + idx));
+  double2 v = make_double2(0.0, 0.0);
+  if (idx < lx) v.x = x[idx];
+  return v;
+}
+
+__device__ __forceinline__ double ld1(const double* x, uint64_t idx, uint64_t lx) {
+  return idx < lx ? x[idx] : 0.0;
+}
+
+// w even, w*h < 2^32, x and y 16-byte aligned.  m = cells that execute.
+__global__ void __launch_bounds__(kThreads) k_stencil2d_march(const double* __restrict__ x,
+                                                              double* __restrict__ y, uint32_t w,
+                                                              uint32_t h, uint64_t m, uint64_t lx,
+                                                              uint32_t col_chunks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint64_t cx = wid % col_chunks, ry = wid / col_chunks;
+  const uint32_t c0 = (uint32_t)cx * 64u;
+  const uint32_t r0 = (uint32_t)ry * kRows;
+  if (r0 >= h) return;  // warp-uniform
+  const uint32_t r1 = (r0 + kRows < h) ? r0 + kRows : h;
+  const uint32_t j = c0 + 2u * (uint32_t)lane;  // my columns j, j+1 (j even)
+  const bool mine = j < w;                      // w even: j < w => j+1 < w
+  // (up, cur) of the first row; rows outside the grid read as 0 (never used)
+  double2 up = make_double2(0.0, 0.0), cur = make_double2(0.0, 0.0);
+  if (mine && r0 > 0) up = ld2(x, (uint64_t)(r0 - 1) * w + j, lx);
+  if (mine) cur = ld2(x, (uint64_t)r0 * w + j, lx);
+  double eL = 0.0, eR = 0.0;  // the strip's outside neighbours (lanes 0 / 31)
+  if (lane == 0 && c0 > 0) eL = ld1(x, (uint64_t)r0 * w + c0 - 1, lx);
+  if (lane == 31 && c0 + 64 < w) eR = ld1(x, (uint64_t)r0 * w + c0 + 64, lx);
+#pragma unroll 4
+  for (uint32_t i = r0; i < r1; ++i) {
+    const uint64_t g = (uint64_t)i * w + j;
+    double2 down = make_double2(0.0, 0.0);
+    if (mine && i + 1 < h) down = ld2(x, g + w, lx);
+    // next row's strip-edge cells, issued early
+    double nL = 0.0, nR = 0.0;
+    if (i + 1 < r1) {
+      if (lane == 0 && c0 > 0) nL = ld1(x, g + w - 1, lx);
+      if (lane == 31 && c0 + 64 < w) nR = ld1(x, g + w + 2, lx);  // j + 2 = c0 + 64
+    }
+    double west = __shfl_up_sync(0xffffffffu, cur.y, 1);
+    double east = __shfl_down_sync(0xffffffffu, cur.x, 1);
+    if (lane == 0) west = eL;
+    if (lane == 31) east = eR;
+    if (mine && g < m) {
+      const bool edge_row = (i == 0) || (i == h - 1);
+      const double o0 = (edge_row || j == 0) ? cur.x : interior(up.x, west, cur.y, down.x);
+      const double o1 = (edge_row || j + 1 == w - 1) ? cur.y : interior(up.y, cur.x, east, down.y);
+      if (g + 1 < m) {
+        __stcs(reinterpret_cast<double2*>(y + g), make_double2(o0, o1));
+      } else {
+        y[g] = o0;
+      }
+    }
+    up = cur;
+    cur = down;
+    eL = nL;
+    eR = nR;
+  }
+}
+
+// Batched form: a warp owns 64 columns x RB rows, issues all RB + 2 row
+// loads (and the strip-edge loads) up front — RB + 2 independent 512-byte
+// requests per warp in flight — then computes and stores the RB rows.  The
+// two halo rows per strip mostly hit L2 (the neighbouring strips load them).
+template <int RB>
+__global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __restrict__ x,
+                                                              double* __restrict__ y, uint32_t w,
+                                                              uint32_t h, uint64_t m, uint64_t lx,
+                                                              uint32_t col_chunks) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint64_t cx = wid % col_chunks, ry = wid / col_chunks;
+  const uint32_t c0 = (uint32_t)cx * 64u;
+  const int64_t r0 = (int64_t)ry * RB;
+  if (r0 >= h) return;  // warp-uniform
+  const uint32_t j = c0 + 2u * (uint32_t)lane;
+  const bool mine = j < w;
+  static_assert(RB <= 32, "one strip-edge value per lane");
+  double2 v[RB + 2];  // rows r0-1 .. r0+RB
+#pragma unroll
+  for (int k = 0; k < RB + 2; ++k) {
+    const int64_t r = r0 - 1 + k;
+    v[k] = (mine && r >= 0 && r < h) ? ld2(x, (uint64_t)r * w + j, lx) : make_double2(0.0, 0.0);
+  }
+  // strip-edge cells: lane k holds x[r0+k][c0-1] and x[r0+k][c0+64]
+  const int64_t re = r0 + lane;
+  const bool erow = lane < RB && re < h;
+  const double eLv = (erow && c0 > 0) ? ld1(x, (uint64_t)re * w + c0 - 1, lx) : 0.0;
+  const double eRv = (erow && c0 + 64 < w) ? ld1(x, (uint64_t)re * w + c0 + 64, lx) : 0.0;
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {
+    const int64_t i = r0 + k;
+    const double2 up = v[k], cur = v[k + 1], down = v[k + 2];
+    double west = __shfl_up_sync(0xffffffffu, cur.y, 1);
+    double east = __shfl_down_sync(0xffffffffu, cur.x, 1);
+    const double wl = __shfl_sync(0xffffffffu, eLv, k);
+    const double er = __shfl_sync(0xffffffffu, eRv, k);
+    if (lane == 0) west = wl;
+    if (lane == 31) east = er;
+    const uint64_t g = (uint64_t)i * w + j;
+    if (i < h && mine && g < m) {
+      const bool edge_row = (i == 0) || (i == (int64_t)h - 1);
+      const double o0 = (edge_row || j == 0) ? cur.x : interior(up.x, west, cur.y, down.x);
+      const double o1 = (edge_row || j + 1 == w - 1) ? cur.y : interior(up.y, cur.x, east, down.y);
+      if (g + 1 < m) {
+        __stcs(reinterpret_cast<double2*>(y + g), make_double2(o0, o1));
+      } else {
+        y[g] = o0;
+      }
+    }
+  }
+}
+
+// One thread per cell, u32 arithmetic exactly as stencil2d.k.
+__global__ void __launch_bounds__(kThreads) k_stencil2d_cells(const double* __restrict__ x,
+                                                              double* __restrict__ y, uint32_t w,
+                                                              uint32_t h, uint64_t m) {
+  const uint64_t t = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (t >= m) return;
+  const uint32_t g = (uint32_t)t;
+  const uint32_t row = g / w;
+  const uint32_t col = g - row * w;
+  if (row == 0 || row == h - 1u || col == 0 || col == w - 1u) {
+    y[g] = x[g];
+  } else {
+    y[g] = interior(x[(uint32_t)(g - w)], x[g - 1u], x[g + 1u], x[(uint32_t)(g + w)]);
+  }
+}
+
+// OFL_STENCIL2D_VARIANT (sweeps): 0 = batch of 8 rows per warp (default,
+// profiles/r01_stencil2d_sweep.txt), 1 = row marching (32 rows), 2/3/4 =
+// batch of 16/4/12 rows
+int stencil2d_variant() {
+  static int v = [] {
+    const char* e = getenv("OFL_STENCIL2D_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+}  // namespace
+
+extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t w, uint32_t h,
+                             uint64_t items, uint64_t x_elems, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (x == y && items) return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil2d: x and y must differ");
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  const uint64_t cells = (uint64_t)(uint32_t)(w * h);  // u32 wrap as stencil2d.k
+  const uint64_t m = items < cells ? items : cells;
+  if (m) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+    const bool fits = (uint64_t)w * h < (1ull << 32);
+    if (aligned && fits && (w & 1u) == 0) {
+      const uint32_t col_chunks = (w + 63u) / 64u;
+      const uint64_t rows_needed = (m + w - 1) / w;  // rows holding executed cells
+      const int v = stencil2d_variant();
+      const uint64_t rows_per_warp = v == 1 ? kRows : v == 2 ? 16 : v == 3 ? 4 : v == 4 ? 12 : 8;
+      const uint64_t row_chunks = (rows_needed + rows_per_warp - 1) / rows_per_warp;
+      const uint64_t warps = (uint64_t)col_chunks * row_chunks;
+      const unsigned blocks = (unsigned)((warps + kThreads / 32 - 1) / (kThreads / 32));
+      cudaStream_t cs = s->cs;
+      if (v == 1)
+        k_stencil2d_march<<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+      else if (v == 2)
+        k_stencil2d_batch<16><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+      else if (v == 3)
+        k_stencil2d_batch<4><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+      else if (v == 4)
+        k_stencil2d_batch<12><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+      else
+        k_stencil2d_batch<8><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+    } else {
+      const uint64_t blocks = (m + kThreads - 1) / kThreads;
+      k_stencil2d_cells<<<(unsigned)blocks, kThreads, 0, s->cs>>>(x, y, w, h, m);
+    }
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return ofl::cuda_error(e, "stencil2d launch");
+    ofl::count_launch();
+  }
+  return q.finish(ticket);
+}

@@ -246,6 +246,36 @@ def overhead_cfg(rt, dev, out):
     out["config5_overhead"] = sweep
 
 
+def stencil2d_cfg(rt, dev, out, w=16384, h=16384):
+    """One stencil2d.k Jacobi step over a 16384^2 f64 grid (2 GiB per
+    buffer): 16 B/cell algorithmic, HBM-bound; K launches ping-ponging."""
+    st = rt.device_objects()[0].stream(0)
+    n = w * h
+    x = np.random.default_rng(20180214).random(n)
+    X, Y = dev.create_buffer(n * 8).get(), dev.create_buffer(n * 8).get()
+    X.enqueue_write(0, x)
+    Y.enqueue_write(0, x)
+    prog = dev.create_program_with_source(kernel_source("stencil2d")).get()
+    prog.build("stencil2d").get()
+    grid = (math.ceil(n / 256), 1, 1)
+    prog.run([X, Y, w, h], "stencil2d", grid, (256, 1, 1))
+    got = Y.enqueue_read(0, n * 8).get()
+    ok = got == oracle.stencil2d(x, w, h, out=x.copy(), threads=0).tobytes()
+    for _ in range(3):
+        prog.run([X, Y, w, h], "stencil2d", grid, (256, 1, 1))
+    t = Timer(st)
+    K = 20
+    t.start()
+    for k in range(K):
+        a, b = (X, Y) if k % 2 == 0 else (Y, X)
+        prog.run([a, b, w, h], "stencil2d", grid, (256, 1, 1))
+    ms = t.stop() / K
+    gbs = 16.0 * n / (ms * 1e-3) / 1e9
+    out["stencil2d"] = {"w": w, "h": h, "kernel_ms": round(ms, 3), "gbs": round(gbs, 1),
+                        "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
+                        "bitexact_one_step": ok}
+
+
 def sum_cfg(rt, dev, out):
     """u32 wrap-around sum (sum.k) at 2^28 elements: 4 B/elem, HBM-bound."""
     st = rt.device_objects()[0].stream(0)
@@ -325,7 +355,8 @@ def partition_cfg(rt, dev, out):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="stream,heat,mandel,dot,sum,overhead,partition,transfer")
+    ap.add_argument("--only",
+                    default="stream,heat,mandel,dot,sum,stencil2d,overhead,partition,transfer")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     with open(os.path.join(REPO, "tests", "golden", "golden.json")) as fh:
@@ -343,7 +374,8 @@ def main():
              "overhead": lambda: overhead_cfg(rt, dev, out),
              "partition": lambda: partition_cfg(rt, dev, out),
              "transfer": lambda: transfer_cfg(rt, dev, out),
-             "sum": lambda: sum_cfg(rt, dev, out)}[name]()
+             "sum": lambda: sum_cfg(rt, dev, out),
+             "stencil2d": lambda: stencil2d_cfg(rt, dev, out)}[name]()
             print(f"[{name}] {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
     text = json.dumps(out, indent=1)
     print(text)

@@ -145,11 +145,60 @@ def lang_cases(dev) -> list:
     return res
 
 
+STENCIL2D_CASES = ((4, 3, 501, None), (5, 4, 502, None), (64, 48, 503, None),
+                   (64, 48, 504, 1000), (63, 47, 505, None), (1, 9, 506, None),
+                   (1024, 768, 507, None), (1000, 601, 508, None))
+
+
+def stencil2d_cases(dev) -> dict:
+    """kernels/stencil2d.k executed by the reference (one step, several grid
+    shapes incl. odd widths, a partial launch) and 20 ping-pong steps."""
+    src = mine("stencil2d")
+    cases = []
+    for w, h, seed, items in STENCIL2D_CASES:
+        x = np.random.default_rng(seed).random(w * h)
+        xb, yb = buf_with(dev, x.tobytes()), dev.create_buffer(w * h * 8).get()
+        # a partial launch must cover exactly `items` work items: block 8
+        run(dev, src, "stencil2d", [xb, yb, w, h], w * h if items is None else items,
+            256 if items is None else 8)
+        raw = yb.enqueue_read_sync(0, w * h * 8)
+        case = {"w": w, "h": h, "seed": seed, "items": items, "sha256": sha(raw)}
+        if w * h <= 64:
+            case["input"] = x.tolist()
+            case["output"] = np.frombuffer(raw, np.float64).tolist()
+        cases.append(case)
+    heat = []
+    for w, h, steps, seed in ((128, 96, 20, 511), (257, 130, 7, 512)):
+        x = np.random.default_rng(seed).random(w * h)
+        a, b = buf_with(dev, x.tobytes()), dev.create_buffer(w * h * 8).get()
+        prog = dev.create_program_with_source(src).get()
+        prog.build("stencil2d").get(timeout=600)
+        grid = (math.ceil(w * h / 256), 1, 1)
+        for s in range(steps):
+            s_, d_ = (a, b) if s % 2 == 0 else (b, a)
+            prog.run([s_, d_, w, h], "stencil2d", grid, (256, 1, 1))
+        final = a if steps % 2 == 0 else b
+        heat.append({"w": w, "h": h, "steps": steps, "seed": seed,
+                     "sha256": sha(final.enqueue_read_sync(0, w * h * 8))})
+    return {"step": cases, "heat": heat}
+
+
 def main() -> None:
+    if "--only-stencil2d" in sys.argv:  # add/refresh one section in place
+        path = os.path.join(HERE, "golden.json")
+        with open(path) as fh:
+            out = json.load(fh)
+        with Runtime(backend="host") as rt:
+            out["stencil2d"] = stencil2d_cases(rt.get_all_devices().get()[0])
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+        print("updated stencil2d in golden.json")
+        return
     out: dict = {"generator": "tests/golden/make_golden.py", "reference": "offloadrt (host backend)"}
     t0 = time.time()
     with Runtime(backend="host") as rt:
         dev = rt.get_all_devices().get()[0]
+        out["stencil2d"] = stencil2d_cases(dev)
 
         # -- stencil: hand case + random sizes (test_acceptance.py:62-66) ----
         cases = []

@@ -70,6 +70,18 @@ def test_new_buffer_reads_zero(dev):
     assert buf.enqueue_read_sync(0, 4000) == bytes(4000)
 
 
+def test_out_of_memory_fails_the_token(dev):
+    """A request beyond the 180 GB of HBM fails the create_buffer token with
+    OutOfMemoryError (reference: the device's capacity check fails the
+    token, device.py:217-228); the device stays usable."""
+    from paper_1810_11482_b200 import OutOfMemoryError
+
+    tok = dev.create_buffer(1 << 40)  # 1 TiB
+    with pytest.raises(OutOfMemoryError):
+        tok.get(timeout=60)
+    assert dev.create_buffer(64).get().size_bytes == 64
+
+
 def test_create_size_zero_rejected(dev):
     with pytest.raises(BadArgsError):
         dev.create_buffer(0)

@@ -47,6 +47,29 @@ def test_heat_steps(golden, idx):
         assert sha(npo.heat(x, case["steps"])) == case["sha256"]
 
 
+@pytest.mark.parametrize("idx", range(8))
+def test_stencil2d_step(golden, idx):
+    """stencil2d.k as the reference executes it: grids with odd widths, a
+    1-wide grid, a partial launch (items < w*h leaves the rest zero)."""
+    case = golden["stencil2d"]["step"][idx]
+    w, h = case["w"], case["h"]
+    x = np.random.default_rng(case["seed"]).random(w * h)
+    y = oracle.stencil2d(x, w, h, items=case["items"], threads=0)
+    assert sha(y) == case["sha256"]
+    if case["items"] is None:
+        assert sha(npo.stencil2d(x, w, h)) == case["sha256"]
+    if "output" in case:
+        assert x.tolist() == case["input"] and y.tolist() == case["output"]
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_heat2d_steps(golden, idx):
+    case = golden["stencil2d"]["heat"][idx]
+    w, h = case["w"], case["h"]
+    x = np.random.default_rng(case["seed"]).random(w * h)
+    assert sha(oracle.heat2d(x, w, h, case["steps"], threads=0)) == case["sha256"]
+
+
 def test_sum_known_answers(golden):
     for case in golden["sum"]:
         if "values" in case:
