@@ -153,6 +153,15 @@ int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n, uint64_t 
  * launch; see bindings._stencil2d_oob). */
 int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t w, uint32_t h,
                   uint64_t items, uint64_t x_elems, uint64_t* ticket);
+/* One stencil2d.k step of a row slab (w x h local rows incl. ghost rows)
+ * for the multi-GPU 2-D heat equation: writes only the owned rows
+ * [own_lo, own_hi) of y, and stores the first / last owned row straight into
+ * up_ghost[0..w) / down_ghost[0..w) — the neighbouring slabs' ghost rows on
+ * devices up_dev / down_dev (NVLink peer stores; NULL = no neighbour).  The
+ * caller orders each step after the neighbours' previous step. */
+int ofl_stencil2d_slab(ofl_stream* s, const double* x, double* y, uint32_t w, uint32_t h,
+                       uint32_t own_lo, uint32_t own_hi, double* up_ghost, int up_dev,
+                       double* down_ghost, int down_dev, uint64_t* ticket);
 /* `steps` applications of stencil.k ping-ponging x <-> y (heat equation,
  * BASELINE config 2); the final state is in x if steps is even else in y.
  * Temporal blocking: `tb` steps are fused per pass through HBM (1 = none). */

@@ -519,6 +519,88 @@ class HeatSlabs:
         return out
 
 
+class Heat2DSlabs:
+    """Row-slab decomposition of the 2-D heat equation (kernels/stencil2d.k)
+    over several devices in this process.  Slab g holds its owned rows plus
+    one ghost row on each inner side; each step is one ``ofl_stencil2d_slab``
+    launch per device that writes the owned rows and stores its first / last
+    owned row straight into the neighbours' ghost rows (NVLink peer stores),
+    ordered after the neighbours' previous step by cross-device events —
+    the same fused exchange as the 1-D ``HeatSlabs``."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], x: np.ndarray, w: int, h: int):
+        G = len(devices)
+        x = np.asarray(x, dtype=np.float64).reshape(h, w)
+        try:
+            self.layout = decomp.slabs(h, G, 1)
+        except ValueError as exc:
+            raise BadArgsError(str(exc)) from None
+        self.devices, self.w, self.h = list(devices), w, h
+        self.bounds = decomp.shard_bounds(h, G)
+        self.a, self.b = [], []
+        for g, d in enumerate(self.devices):
+            sl = self.layout[g]
+            local = np.ascontiguousarray(x[sl.start : sl.start + sl.length])
+            A = d.create_buffer(local.nbytes).get()
+            B = d.create_buffer(local.nbytes).get()
+            A.enqueue_write(0, local.tobytes())
+            B.enqueue_write(0, local.tobytes())
+            self.a.append(A)
+            self.b.append(B)
+
+    def run(self, steps: int):
+        import ctypes
+
+        from .. import _native
+
+        objs = lambda hs: [h_._runtime.local._buffer(h_.gid) for h_ in hs]  # noqa: E731
+        cur_h, nxt_h = self.a, self.b
+        cur, nxt = objs(cur_h), objs(nxt_h)
+        G, lay, w = len(self.devices), self.layout, self.w
+        streams = [o.device.stream(0) for o in cur]
+        ords = [o.device.ordinal for o in cur]
+        lib = streams[0].lib
+        prev = [0] * G
+        ticket = ctypes.c_uint64()
+        for _ in range(steps):
+            now = []
+            for g in range(G):
+                st = streams[g]
+                for nb in (g - 1, g + 1):
+                    if 0 <= nb < G and prev[nb]:
+                        _native.check(lib.ofl_stream_wait(st.ptr, streams[nb].ptr, prev[nb]),
+                                      "halo ordering")
+                sl = lay[g]
+                up = (nxt[g - 1].ptr + (lay[g - 1].left + lay[g - 1].owned) * w * 8) if g else None
+                down = nxt[g + 1].ptr if g + 1 < G else None
+                _native.check(lib.ofl_stencil2d_slab(
+                    st.ptr, cur[g].ptr, nxt[g].ptr, w, sl.length, sl.left, sl.left + sl.owned,
+                    up, ords[g - 1] if g else -1, down, ords[g + 1] if g + 1 < G else -1,
+                    ctypes.byref(ticket)), "stencil2d slab step")
+                now.append(ticket.value)
+            prev = now
+            cur, nxt, cur_h, nxt_h = nxt, cur, nxt_h, cur_h
+        self.a, self.b = cur_h, nxt_h
+        return when_all([streams[g].token(prev[g]) for g in range(G)]) if steps else None
+
+    def gather(self) -> np.ndarray:
+        out = np.empty((self.h, self.w))
+        reads = []
+        for g, sl in enumerate(self.layout):
+            reads.append((g, self.a[g].enqueue_read(sl.left * self.w * 8, sl.owned * self.w * 8)))
+        for g, t in reads:
+            out[self.bounds[g] : self.bounds[g + 1]] = np.frombuffer(t.get(), np.float64).reshape(
+                -1, self.w)
+        return out.ravel()
+
+
+def heat2d_multi(devices: Sequence[DeviceHandle], x: np.ndarray, w: int, h: int,
+                 steps: int) -> np.ndarray:
+    slabs = Heat2DSlabs(devices, x, w, h)
+    slabs.run(steps)
+    return slabs.gather()
+
+
 def heat_multi(devices: Sequence[DeviceHandle], x: np.ndarray, steps: int, halo: int = 1,
                fused: Optional[bool] = None) -> np.ndarray:
     slabs = HeatSlabs(devices, np.asarray(x, dtype=np.float64), halo, fused)

@@ -32,6 +32,15 @@ __device__ __forceinline__ double interior(double n, double w, double e, double 
   return __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(n, w), e), s));
 }
 
+// Multi-GPU row slabs (ofl_stencil2d_slab): only the owned local rows
+// [own_lo, own_hi) are written; the first / last owned row also goes
+// straight into the neighbouring slabs' ghost rows (peer stores over NVLink).
+struct SlabRows {
+  int64_t own_lo, own_hi;
+  double* up;    // receives row own_lo (w cells), or null
+  double* down;  // receives row own_hi - 1, or null
+};
+
 __device__ __forceinline__ double2 ld2(const double* x, uint64_t idx, uint64_t lx) {
   // idx is even (16-byte aligned pair); either half may lie past the buffer
   if (idx + 1 < lx) return __ldcs(reinterpret_cast<const double2*>(x + idx));
@@ -101,11 +110,12 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_march(const double* __re
 // loads (and the strip-edge loads) up front — RB + 2 independent 512-byte
 // requests per warp in flight — then computes and stores the RB rows.  The
 // two halo rows per strip mostly hit L2 (the neighbouring strips load them).
-template <int RB>
+template <int RB, bool kSlab = false>
 __global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __restrict__ x,
                                                               double* __restrict__ y, uint32_t w,
                                                               uint32_t h, uint64_t m, uint64_t lx,
-                                                              uint32_t col_chunks) {
+                                                              uint32_t col_chunks,
+                                                              SlabRows sr = SlabRows{}) {
   const int lane = threadIdx.x & 31;
   const uint64_t wid = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const uint64_t cx = wid % col_chunks, ry = wid / col_chunks;
@@ -141,7 +151,14 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __re
       const bool edge_row = (i == 0) || (i == (int64_t)h - 1);
       const double o0 = (edge_row || j == 0) ? cur.x : interior(up.x, west, cur.y, down.x);
       const double o1 = (edge_row || j + 1 == w - 1) ? cur.y : interior(up.y, cur.x, east, down.y);
-      if (g + 1 < m) {
+      if (kSlab) {
+        if (i >= sr.own_lo && i < sr.own_hi) {
+          const double2 o = make_double2(o0, o1);
+          __stcs(reinterpret_cast<double2*>(y + g), o);
+          if (sr.up && i == sr.own_lo) *reinterpret_cast<double2*>(sr.up + j) = o;
+          if (sr.down && i == sr.own_hi - 1) *reinterpret_cast<double2*>(sr.down + j) = o;
+        }
+      } else if (g + 1 < m) {
         __stcs(reinterpret_cast<double2*>(y + g), make_double2(o0, o1));
       } else {
         y[g] = o0;
@@ -151,18 +168,27 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __re
 }
 
 // One thread per cell, u32 arithmetic exactly as stencil2d.k.
+template <bool kSlab = false>
 __global__ void __launch_bounds__(kThreads) k_stencil2d_cells(const double* __restrict__ x,
                                                               double* __restrict__ y, uint32_t w,
-                                                              uint32_t h, uint64_t m) {
+                                                              uint32_t h, uint64_t m,
+                                                              SlabRows sr = SlabRows{}) {
   const uint64_t t = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   if (t >= m) return;
   const uint32_t g = (uint32_t)t;
   const uint32_t row = g / w;
   const uint32_t col = g - row * w;
+  if (kSlab && (row < sr.own_lo || row >= sr.own_hi)) return;
+  double v;
   if (row == 0 || row == h - 1u || col == 0 || col == w - 1u) {
-    y[g] = x[g];
+    v = x[g];
   } else {
-    y[g] = interior(x[(uint32_t)(g - w)], x[g - 1u], x[g + 1u], x[(uint32_t)(g + w)]);
+    v = interior(x[(uint32_t)(g - w)], x[g - 1u], x[g + 1u], x[(uint32_t)(g + w)]);
+  }
+  y[g] = v;
+  if (kSlab) {
+    if (sr.up && row == sr.own_lo) sr.up[col] = v;
+    if (sr.down && row == sr.own_hi - 1) sr.down[col] = v;
   }
 }
 
@@ -215,6 +241,41 @@ extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t
     }
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return ofl::cuda_error(e, "stencil2d launch");
+    ofl::count_launch();
+  }
+  return q.finish(ticket);
+}
+
+extern "C" int ofl_stencil2d_slab(ofl_stream* s, const double* x, double* y, uint32_t w,
+                                  uint32_t h, uint32_t own_lo, uint32_t own_hi, double* up_ghost,
+                                  int up_dev, double* down_ghost, int down_dev,
+                                  uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (x == y) return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil2d slab: x and y must differ");
+  if ((uint64_t)w * h >= (1ull << 32) || own_lo > own_hi || own_hi > h)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil2d slab: bad shape or owned rows");
+  if (up_ghost && up_dev != s->dev) ofl::enable_peer(s->dev, up_dev);
+  if (down_ghost && down_dev != s->dev) ofl::enable_peer(s->dev, down_dev);
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  const uint64_t m = (uint64_t)w * h;
+  if (m && own_lo < own_hi) {
+    SlabRows sr{(int64_t)own_lo, (int64_t)own_hi, up_ghost, down_ghost};
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                           reinterpret_cast<uintptr_t>(up_ghost) |
+                           reinterpret_cast<uintptr_t>(down_ghost)) & 15) == 0;
+    if (aligned && (w & 1u) == 0) {
+      constexpr int RB = 8;
+      const uint32_t col_chunks = (w + 63u) / 64u;
+      const uint64_t warps = (uint64_t)col_chunks * ((h + RB - 1) / RB);
+      const unsigned blocks = (unsigned)((warps + kThreads / 32 - 1) / (kThreads / 32));
+      k_stencil2d_batch<RB, true><<<blocks, kThreads, 0, s->cs>>>(x, y, w, h, m, m, col_chunks, sr);
+    } else {
+      const unsigned blocks = (unsigned)((m + kThreads - 1) / kThreads);
+      k_stencil2d_cells<true><<<blocks, kThreads, 0, s->cs>>>(x, y, w, h, m, sr);
+    }
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return ofl::cuda_error(e, "stencil2d slab launch");
     ofl::count_launch();
   }
   return q.finish(ticket);

@@ -185,3 +185,20 @@ def test_device_fault_fails_tokens_not_hangs():
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
     assert line == ("then:InternalError kernel:InternalError read:InternalError "
                     "when_all:InternalError new:InternalError"), line
+
+
+@pytest.mark.parametrize("parts,w,h,steps", [(2, 130, 67, 9), (3, 129, 50, 12), (4, 1024, 256, 5),
+                                             (1, 64, 64, 3)])
+def test_heat2d_fused_row_slabs(parts, w, h, steps):
+    """2-D heat over row slabs on concurrently running logical devices, ghost
+    rows refreshed by peer stores from the step kernel; even and odd widths
+    (row-batch and per-cell kernels)."""
+    from paper_1810_11482_b200.bench.harness import heat2d_multi
+
+    import oracle
+
+    x = np.random.default_rng(parts * 100 + w).random(w * h)
+    with Runtime(devices=[0] * parts) as rt:
+        got = heat2d_multi(rt.get_all_devices().get(), x, w, h, steps)
+    exp = oracle.heat2d(x, w, h, steps, threads=0)
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
