@@ -137,7 +137,11 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
     if (!any) break;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      n[p] += live[p];
+      // predicated increment (one instruction; the plain `n += live` form
+      // compiles to add + select + move around the loop back edge)
+      asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}"
+          : "+r"(n[p])
+          : "r"((uint32_t)live[p]));
       const double t = __dadd_rn(__dsub_rn(r2[p], i2[p]), cr[p]);
       zi[p] = FUSED ? __fma_rn(2.0, __dmul_rn(zr[p], zi[p]), ci[p])
                     : __dadd_rn(__dmul_rn(__dmul_rn(2.0, zr[p]), zi[p]), ci[p]);
