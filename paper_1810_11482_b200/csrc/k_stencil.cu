@@ -290,8 +290,18 @@ struct SlabOut {
   double* right;  // receives y[own_hi - h, own_hi), or null
 };
 
+// Four 128-thread CTAs per SM for R <= 24: caps registers at 128 (a few
+// bytes of spill outside the step loop) and lifts residency from 12 to 16
+// warps per SM, which hides the tile loads better (R=24 tb=64: 43.9 ms for
+// config 2 vs 45.2 at 3 CTAs/SM and 51.7 unconstrained at 209 registers).
+// The slab form (extra peer stores) would spill at 128, so it gets three.
+template <int R, bool kSlab>
+constexpr int heat_warp_min_blocks() {
+  return kSlab ? 3 : (R <= 24 ? 4 : 2);
+}
+
 template <int R, bool kSlab = false>
-__global__ void __launch_bounds__(kWarpThreads) k_heat_warp(const double* __restrict__ x,
+__global__ void __launch_bounds__(kWarpThreads, heat_warp_min_blocks<R, kSlab>()) k_heat_warp(const double* __restrict__ x,
                                                             double* __restrict__ y, uint64_t n,
                                                             int tb, bool fma_ok,
                                                             SlabOut so = SlabOut{}) {
