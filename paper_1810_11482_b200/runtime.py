@@ -227,6 +227,26 @@ class Runtime:
             return self.local
         raise UnknownGidError(f"{gid} names an unknown locality")
 
+    def local_program(self, gid: GlobalId):
+        """(registry objects, ProgramObject) for a program owned by this
+        process, else None — the handles' fast launch path (handles.py)."""
+        if gid.locality_id != self.registry.self_locality_id:
+            return None
+        try:
+            return self.registry._objects, self.local._program(gid)
+        except Exception:  # noqa: BLE001 - the general path reports it
+            return None
+
+    def local_buffer(self, gid: GlobalId):
+        """(registry objects, BufferObject) for a buffer owned by this process,
+        else None — the handles' fast write path (handles.py)."""
+        if gid.locality_id != self.registry.self_locality_id:
+            return None
+        try:
+            return self.registry._objects, self.local._buffer(gid)
+        except Exception:  # noqa: BLE001 - the general path reports it
+            return None
+
     def get_all_devices(self, major: int = 0, minor: int = 0) -> CompletionToken:
         """Every device with capability >= (major, minor), in ordinal order."""
         return make_ready(
