@@ -30,7 +30,7 @@ from typing import Any, Callable, Optional
 
 from . import _native
 from .errors import InternalError
-from .futures import _PENDING, CompletionToken, _lock
+from .futures import _PENDING, _READY, DEVICE_TOKEN_TYPES, CompletionToken, _lock
 
 _ids = itertools.count(1)
 _pending: dict[int, "DeviceToken"] = {}
@@ -127,9 +127,16 @@ class DeviceToken(CompletionToken):
                 return
             self._claimed = True
             fin = self._finish
-            self._finish = None
+            if fin is None:  # no host-side work: complete under the same lock
+                self._state = _READY
+                callbacks = self._callbacks
+                self._callbacks = None
+            else:
+                self._finish = None
         if fin is None:
-            self._try_complete(value=None)
+            if callbacks:
+                for cb in callbacks:
+                    cb(self)
             return
         try:
             value = fin()
@@ -201,3 +208,6 @@ class DeviceToken(CompletionToken):
             with _pending_lock:
                 _pending.pop(tid, None)
             self._fail(status, "completion notify failed")
+
+
+DEVICE_TOKEN_TYPES.add(DeviceToken)
