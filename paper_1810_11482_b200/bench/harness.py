@@ -398,6 +398,52 @@ def mandelbrot_multi(devices: Sequence[DeviceHandle], width: int, height: int, m
 # -- heat equation across devices (config 2) ---------------------------------------
 
 
+def _drive_slabs(a_handles: list, b_handles: list, layout: list, unit: int, rounds: list,
+                 launch: Callable, what: str):
+    """Run slab passes with the halo exchange fused into the kernels.
+
+    Round r launches, on every device g (default stream), one pass from its
+    current buffer into the other one; the pass writes its owned cells and
+    peer-stores its first / last boundary strip into the neighbours' ghost
+    cells of *their* next buffer (``unit`` bytes per cell or row).  Each
+    device's pass first waits for its two neighbours' previous pass (RAW on
+    the ghosts it reads, WAR on the ghosts it stores).  Returns the buffers
+    swapped to (current, other) and a token for the last round."""
+    import ctypes
+
+    from .. import _native
+
+    def objs(handles):
+        return [h._runtime.local._buffer(h.gid) for h in handles]
+
+    cur_h, nxt_h = list(a_handles), list(b_handles)
+    cur, nxt = objs(cur_h), objs(nxt_h)
+    G = len(layout)
+    streams = [o.device.stream(0) for o in cur]
+    ords = [o.device.ordinal for o in cur]
+    lib = streams[0].lib
+    prev = [0] * G
+    ticket = ctypes.c_uint64()
+    for arg in rounds:
+        now = []
+        for g in range(G):
+            st = streams[g]
+            for nb in (g - 1, g + 1):
+                if 0 <= nb < G and prev[nb]:
+                    _native.check(lib.ofl_stream_wait(st.ptr, streams[nb].ptr, prev[nb]),
+                                  "halo ordering")
+            up = (nxt[g - 1].ptr + (layout[g - 1].left + layout[g - 1].owned) * unit) if g else None
+            down = nxt[g + 1].ptr if g + 1 < G else None
+            _native.check(launch(lib, st, cur[g], nxt[g], layout[g], up, ords[g - 1] if g else -1,
+                                 down, ords[g + 1] if g + 1 < G else -1, arg,
+                                 ctypes.byref(ticket)), what)
+            now.append(ticket.value)
+        prev = now
+        cur, nxt, cur_h, nxt_h = nxt, cur, nxt_h, cur_h
+    tok = when_all([streams[g].token(prev[g]) for g in range(G)]) if rounds else None
+    return cur_h, nxt_h, tok
+
+
 class HeatSlabs:
     """1-D slab decomposition of the heat equation over several devices.
 
@@ -471,42 +517,16 @@ class HeatSlabs:
         return when_all(toks) if toks else None
 
     def _run_fused(self, steps: int):
-        import ctypes
+        h = self.halo
+        ks = [min(h, steps - done) for done in range(0, steps, h)]
 
-        from .. import _native
+        def launch(lib, st, cur, nxt, sl, up, up_dev, down, down_dev, k, ticket):
+            return lib.ofl_heat_slab(st.ptr, cur.ptr, nxt.ptr, sl.length, k, sl.left,
+                                     sl.left + sl.owned, up, up_dev, down, down_dev, h, ticket)
 
-        objs = lambda hs: [h._runtime.local._buffer(h.gid) for h in hs]  # noqa: E731
-        cur_h, nxt_h = self.a, self.b
-        cur, nxt = objs(cur_h), objs(nxt_h)
-        G, lay, h = len(self.devices), self.layout, self.halo
-        streams = [o.device.stream(0) for o in cur]
-        ords = [o.device.ordinal for o in cur]
-        lib = streams[0].lib
-        prev = [0] * G
-        ticket = ctypes.c_uint64()
-        left = steps
-        while left > 0:
-            k = min(h, left)
-            now = []
-            for g in range(G):
-                st = streams[g]
-                for nb in (g - 1, g + 1):
-                    if 0 <= nb < G and prev[nb]:
-                        _native.check(lib.ofl_stream_wait(st.ptr, streams[nb].ptr, prev[nb]),
-                                      "halo ordering")
-                own_lo = lay[g].left
-                lghost = (nxt[g - 1].ptr + (lay[g - 1].left + lay[g - 1].owned) * 8) if g else None
-                rghost = nxt[g + 1].ptr if g + 1 < G else None
-                _native.check(lib.ofl_heat_slab(
-                    st.ptr, cur[g].ptr, nxt[g].ptr, lay[g].length, k, own_lo, own_lo + lay[g].owned,
-                    lghost, ords[g - 1] if g else -1, rghost, ords[g + 1] if g + 1 < G else -1, h,
-                    ctypes.byref(ticket)), "heat slab pass")
-                now.append(ticket.value)
-            prev = now
-            cur, nxt, cur_h, nxt_h = nxt, cur, nxt_h, cur_h
-            left -= k
-        self.a, self.b = cur_h, nxt_h
-        return when_all([streams[g].token(prev[g]) for g in range(G)]) if steps else None
+        self.a, self.b, tok = _drive_slabs(self.a, self.b, self.layout, 8, ks, launch,
+                                           "heat slab pass")
+        return tok
 
     def gather(self) -> np.ndarray:
         out = np.empty(self.n)
@@ -549,39 +569,15 @@ class Heat2DSlabs:
             self.b.append(B)
 
     def run(self, steps: int):
-        import ctypes
+        w = self.w
 
-        from .. import _native
+        def launch(lib, st, cur, nxt, sl, up, up_dev, down, down_dev, _arg, ticket):
+            return lib.ofl_stencil2d_slab(st.ptr, cur.ptr, nxt.ptr, w, sl.length, sl.left,
+                                          sl.left + sl.owned, up, up_dev, down, down_dev, ticket)
 
-        objs = lambda hs: [h_._runtime.local._buffer(h_.gid) for h_ in hs]  # noqa: E731
-        cur_h, nxt_h = self.a, self.b
-        cur, nxt = objs(cur_h), objs(nxt_h)
-        G, lay, w = len(self.devices), self.layout, self.w
-        streams = [o.device.stream(0) for o in cur]
-        ords = [o.device.ordinal for o in cur]
-        lib = streams[0].lib
-        prev = [0] * G
-        ticket = ctypes.c_uint64()
-        for _ in range(steps):
-            now = []
-            for g in range(G):
-                st = streams[g]
-                for nb in (g - 1, g + 1):
-                    if 0 <= nb < G and prev[nb]:
-                        _native.check(lib.ofl_stream_wait(st.ptr, streams[nb].ptr, prev[nb]),
-                                      "halo ordering")
-                sl = lay[g]
-                up = (nxt[g - 1].ptr + (lay[g - 1].left + lay[g - 1].owned) * w * 8) if g else None
-                down = nxt[g + 1].ptr if g + 1 < G else None
-                _native.check(lib.ofl_stencil2d_slab(
-                    st.ptr, cur[g].ptr, nxt[g].ptr, w, sl.length, sl.left, sl.left + sl.owned,
-                    up, ords[g - 1] if g else -1, down, ords[g + 1] if g + 1 < G else -1,
-                    ctypes.byref(ticket)), "stencil2d slab step")
-                now.append(ticket.value)
-            prev = now
-            cur, nxt, cur_h, nxt_h = nxt, cur, nxt_h, cur_h
-        self.a, self.b = cur_h, nxt_h
-        return when_all([streams[g].token(prev[g]) for g in range(G)]) if steps else None
+        self.a, self.b, tok = _drive_slabs(self.a, self.b, self.layout, w * 8, [None] * steps,
+                                           launch, "stencil2d slab step")
+        return tok
 
     def gather(self) -> np.ndarray:
         out = np.empty((self.h, self.w))
