@@ -97,6 +97,35 @@ def stream_cfg(rt, dev, out):
         res[op] = {"n": n, "us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
                    "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
                    "frac_8tbs_spec": round(gbs / 8000.0, 4), "bitexact": ok}
+    # size sweep: N = 2^22 .. 2^30, triad, back-to-back launches;
+    # 3 x 8 x N bytes <= L2 (126 MB) only at 2^22 — those launches run from L2
+    sweep = {}
+    l2 = rt.device_objects()[0].physical.l2_bytes
+    prog.build("triad").get()
+    for lg in range(22, 31):
+        m = 1 << lg
+        As, Bs, Cs = (dev.create_buffer(m * 8).get() for _ in range(3))
+        Bs.enqueue_write(0, np.full(m, 0.5))
+        Cs.enqueue_write(0, np.full(m, 0.25))
+        args = [As, Bs, Cs, 3.0, m]
+        grid = ((m + 255) // 256, 1, 1)
+        for _ in range(5):
+            prog.run(args, "triad", grid, (256, 1, 1))
+        K = max(10, min(1000, (1 << 32) // (24 * m) * 10))
+        t = Timer(st)
+        t.start()
+        for _ in range(K):
+            prog.run(args, "triad", grid, (256, 1, 1))
+        ms = t.stop() / K
+        gbs = 24.0 * m / (ms * 1e-3) / 1e9
+        ok = bool(np.all(np.frombuffer(As.enqueue_read(0, 8 * min(m, 1 << 16)).get(),
+                                       np.float64) == 0.5 + 3.0 * 0.25))
+        sweep[f"2^{lg}"] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
+                            "frac_measured_hbm": round(gbs / peaks()["hbm_gbs"], 4),
+                            "working_set_mb": round(24 * m / 1e6, 1), "check": ok}
+        del As, Bs, Cs
+    res["triad_size_sweep"] = sweep
+    res["l2_bytes"] = l2
     out["config1_stream"] = res
 
 
