@@ -305,6 +305,52 @@ def stencil2d_cfg(rt, dev, out, w=16384, h=16384):
                         "bitexact_one_step": ok}
 
 
+def cpu_cfg(rt, dev, out):
+    """The CPU restatement of the reference path (oracle/, C, no FMA) timed
+    on this box's host cores for every config, 1 thread (the reference runs
+    each launch on one core, codegen.py:118-123) and all threads, on bounded
+    samples scaled to the full config (stated per entry)."""
+    import os as _os
+
+    T = oracle.max_threads()
+    res = {"threads_all": T, "cpu_count": _os.cpu_count()}
+
+    def timed(fn):
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    n = 1 << 25
+    b, c = np.random.default_rng(1).random(n), np.random.default_rng(2).random(n)
+    a = np.empty(n)
+    oracle.stream("triad", b, c, 3.0, out=a, threads=T)
+    for th in (1, T):
+        sec = min(timed(lambda: oracle.stream("triad", b, c, 3.0, out=a, threads=th))
+                  for _ in range(3))
+        res[f"triad_2^25_t{th}"] = {"ms": round(sec * 1e3, 2), "gbs": round(24 * n / sec / 1e9, 2)}
+    x = np.random.default_rng(3).random(1 << 28)
+    for th in (1, T):
+        sec = timed(lambda: oracle.heat(x, 2, threads=th))
+        res[f"heat_2^28_t{th}"] = {"sample": "2 steps", "ms_per_step": round(sec / 2 * 1e3, 1),
+                                   "extrapolated_1000_steps_s": round(sec / 2 * 1000, 1)}
+    del x
+    w, h, it = 7680, 4320, 2000
+    rows = 96  # 1/45 of the image, cyclic rows so the sample is representative
+    for th in (1, T):
+        sec = timed(lambda: oracle.mandelbrot(w, h, max_iter=it, row_first=0, row_step=h // rows,
+                                              threads=th))
+        res[f"mandelbrot_t{th}"] = {"sample": f"{rows} of {h} rows (cyclic)",
+                                    "extrapolated_s": round(sec * h / rows, 1)}
+    m = 1 << 28
+    fa = np.random.default_rng(4).random(m, dtype=np.float32)
+    fb = np.random.default_rng(5).random(m, dtype=np.float32)
+    for th in (1, T):
+        sec = timed(lambda: oracle.dot_f32(fa, fb, threads=th))
+        res[f"dot_f32_t{th}"] = {"sample": "2^28 elements", "extrapolated_2^31_ms":
+                                 round(sec * 8 * 1e3, 1), "gbs": round(8 * m / sec / 1e9, 2)}
+    out["cpu_reference_port"] = res
+
+
 def sum_cfg(rt, dev, out):
     """u32 wrap-around sum (sum.k) at 2^28 elements: 4 B/elem, HBM-bound."""
     st = rt.device_objects()[0].stream(0)
@@ -385,7 +431,7 @@ def partition_cfg(rt, dev, out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only",
-                    default="stream,heat,mandel,dot,sum,stencil2d,overhead,partition,transfer")
+                    default="stream,heat,mandel,dot,sum,stencil2d,overhead,partition,transfer,cpu")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     with open(os.path.join(REPO, "tests", "golden", "golden.json")) as fh:
@@ -404,7 +450,8 @@ def main():
              "partition": lambda: partition_cfg(rt, dev, out),
              "transfer": lambda: transfer_cfg(rt, dev, out),
              "sum": lambda: sum_cfg(rt, dev, out),
-             "stencil2d": lambda: stencil2d_cfg(rt, dev, out)}[name]()
+             "stencil2d": lambda: stencil2d_cfg(rt, dev, out),
+             "cpu": lambda: cpu_cfg(rt, dev, out)}[name]()
             print(f"[{name}] {time.time() - t0:.1f}s", file=sys.stderr, flush=True)
     text = json.dumps(out, indent=1)
     print(text)
