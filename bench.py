@@ -477,7 +477,7 @@ def run_ours(args) -> None:
                 "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
                 "traffic": traffic,
                 "peak_source": peak_src,
-                "kernel": "k_stream_tile<TRIAD,512,1> (csrc/k_stream.cu)",
+                "kernel": "k_stream_tile<TRIAD,512,1,PDL> (csrc/k_stream.cu; programmatic dependent launch)",
                 "algorithmic_bytes_per_launch": step_bytes,
                 "avg_launch_us": round(avg_launch_ms * 1e3, 3),
             },

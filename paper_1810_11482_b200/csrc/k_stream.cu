@@ -84,12 +84,19 @@ __global__ void __launch_bounds__(T, MINB) k_stream_vec(double* __restrict__ a,
 
 // Tile form: one CTA per contiguous tile of T*U double2, no loop; the
 // hardware block scheduler load-balances the (many) tiles.
-template <int OP, int T, int U>
+template <int OP, int T, int U, bool kPDL = false>
 __global__ void __launch_bounds__(T) k_stream_tile(double* __restrict__ a,
                                                   const double* __restrict__ b,
                                                   const double* __restrict__ c, double s,
                                                   uint64_t n) {
   constexpr bool kC = (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD);
+  if constexpr (kPDL) {
+    // programmatic dependent launch: let the next grid on the stream start
+    // launching its CTAs while this one drains, and wait here until the
+    // previous grid has completed and its memory is visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const uint64_t n2 = n >> 1;
   double2* __restrict__ a2 = reinterpret_cast<double2*>(a);
   const double2* __restrict__ b2 = reinterpret_cast<const double2*>(b);
@@ -218,6 +225,24 @@ void launch_tile(cudaStream_t st, double* a, const double* b, const double* c, d
   k_stream_tile<OP, T, U><<<(unsigned)blocks, T, 0, st>>>(a, b, c, s, n);
 }
 
+template <int OP, int T, int U>
+void launch_tile_pdl(cudaStream_t st, double* a, const double* b, const double* c, double s,
+                     uint64_t n) {
+  uint64_t blocks = ((n >> 1) + (uint64_t)T * U - 1) / ((uint64_t)T * U);
+  if (blocks == 0) blocks = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(T);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_stream_tile<OP, T, U, true>, a, b, c, s, n);
+}
+
 // Launch-shape variants (OFL_STREAM_VARIANT, for tuning sweeps); the default
 // is the one measured fastest on B200 (profiles/).
 int stream_variant() {
@@ -260,19 +285,32 @@ cudaError_t launch(cudaStream_t st, int sms, double* a, const double* b, const d
       k_stream_tma<OP, 2048><<<(unsigned)(blocks ? blocks : 1), kTmaThreads, 0, st>>>(a, b, c, s, n);
       break;
     }
+    case 18:
+      if constexpr (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD)
+        launch_tile_pdl<OP, 512, 1>(st, a, b, c, s, n);
+      else
+        launch_tile_pdl<OP, 512, 2>(st, a, b, c, s, n);
+      break;
     case 17: {
       const uint64_t blocks = (n + 1023) / 1024;
       k_stream_tma<OP, 1024><<<(unsigned)(blocks ? blocks : 1), kTmaThreads, 0, st>>>(a, b, c, s, n);
       break;
     }
-    default:
-      // measured best on B200 (profiles/r01_stream_sweep.txt): one-shot tiles,
-      // 512 threads; 1 double2 per input per thread for the 2-input ops,
-      // 2 for the 1-input ops
+    case 19:  // the default shape without programmatic dependent launch
       if constexpr (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD)
         launch_tile<OP, 512, 1>(st, a, b, c, s, n);
       else
         launch_tile<OP, 512, 2>(st, a, b, c, s, n);
+      break;
+    default:
+      // measured best on B200 (profiles/r01_stream_sweep.txt): one-shot tiles,
+      // 512 threads; 1 double2 per input per thread for the 2-input ops,
+      // 2 for the 1-input ops; launched with programmatic dependent launch so
+      // back-to-back launches overlap CTA scheduling with the previous drain
+      if constexpr (OP == OFL_STREAM_ADD || OP == OFL_STREAM_TRIAD)
+        launch_tile_pdl<OP, 512, 1>(st, a, b, c, s, n);
+      else
+        launch_tile_pdl<OP, 512, 2>(st, a, b, c, s, n);
       break;
   }
   return cudaPeekAtLastError();
