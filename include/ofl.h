@@ -200,6 +200,20 @@ int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double* res, uint
 
 /* partition.k (bench/kernels/partition.k:3-8):
  * out[i] = sqrt(sin(v)^2 + cos(v)^2), v = f64((offset + i) mod 2^32), i < count */
+/* Fused dot product + allreduce over `nranks` devices driven by this process
+ * (BASELINE config 4 without NCCL): rank `rank` reduces its shard like
+ * ofl_dot_f32, then its last CTA stores the fp64 partial into slot `rank` of
+ * every rank's exchange block (xchg[r], ofl_xchg_bytes() bytes of zeroed
+ * device memory on device devs[r]; NVLink peer stores), bumps every rank's
+ * arrival counter (system-scope atomics), waits for all partials of round
+ * `round` (0, 1, 2, ... per call on the group) and sums them in rank order,
+ * so every rank's res[0] holds the identical total.  A rank that waits
+ * longer than 20 s writes NaN and sets the block's status word. */
+#define OFL_MAX_PEER_RANKS 16
+int ofl_xchg_bytes(void);
+int ofl_dot_f32_allreduce(ofl_stream* s, const float* a, const float* b, double* res, uint64_t n,
+                          int rank, int nranks, void* const* xchg, const int* devs,
+                          uint64_t round, uint64_t* ticket);
 int ofl_partition(ofl_stream* s, double* out, uint32_t offset, uint64_t count,
                   uint64_t* ticket);
 

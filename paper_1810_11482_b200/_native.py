@@ -87,6 +87,9 @@ _SIGNATURES = {
                               c_uint64, _u64p]),
     "ofl_stencil2d_slab": (c_int, [_c_stream, c_void_p, c_void_p, c_uint32, c_uint32, c_uint32,
                                    c_uint32, c_void_p, c_int, c_void_p, c_int, _u64p]),
+    "ofl_xchg_bytes": (c_int, []),
+    "ofl_dot_f32_allreduce": (c_int, [_c_stream, c_void_p, c_void_p, c_void_p, c_uint64, c_int,
+                                      c_int, POINTER(c_void_p), POINTER(c_int), c_uint64, _u64p]),
     "ofl_heat_slab": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, c_int, c_uint64, c_uint64,
                               c_void_p, c_int, c_void_p, c_int, c_uint64, _u64p]),
     "ofl_mandelbrot": (

@@ -664,10 +664,18 @@ def run_stream(op: str, n: int, device: DeviceHandle, protocol: TimingProtocol =
 
 class DotShards:
     """a, b split contiguously over the devices; each device reduces its
-    shard to one fp64 partial (dot_f32 builtin) and an NCCL allreduce on the
-    same stream leaves the total on every device."""
+    shard to one fp64 partial.  Combining the partials:
 
-    def __init__(self, devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None):
+    * ``fused`` (default for several physical GPUs in this process, no ``comm``):
+      the reduction kernel's last CTA exchanges the partials with the other
+      devices over NVLink peer memory and sums them in rank order
+      (``collectives.PeerGroup``) — one kernel per device, no collective call;
+    * ``comm`` (a ``collectives.Communicator``): the dot_f32 builtin, then
+      one NCCL allreduce on the same stream;
+    * neither: partials summed on the host."""
+
+    def __init__(self, devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None,
+                 fused: Optional[bool] = None):
         G = len(devices)
         n = a.size
         self.devices = list(devices)
@@ -686,8 +694,20 @@ class DotShards:
             self.R.append(d.create_buffer(8).get())
         self.progs = [_builtin(d, "dot_f32") for d in self.devices]
         self.comm = comm
+        if fused is None:  # default: distinct physical GPUs and no communicator
+            ords = {d._runtime.local._device(d.gid).ordinal for d in self.devices}
+            fused = comm is None and G > 1 and len(ords) == G
+        self.fused = bool(fused)
+        self.group = None
+        if self.fused:
+            from ..collectives import PeerGroup
+
+            self.group = PeerGroup(self.devices[0]._runtime, self.devices)
 
     def enqueue(self):
+        if self.fused:
+            counts = [self.bounds[g + 1] - self.bounds[g] for g in range(len(self.devices))]
+            return self.group.dot_f32(self.A, self.B, self.R, counts)
         for g, p in enumerate(self.progs):
             m = self.bounds[g + 1] - self.bounds[g]
             p.run([self.A[g], self.B[g], self.R[g], m], "dot_f32", (max(1, math.ceil(m / 256)), 1, 1),
@@ -697,12 +717,13 @@ class DotShards:
         return None
 
     def result(self) -> float:
-        if self.comm is None:
+        if self.comm is None and not self.fused:
             return float(sum(np.frombuffer(r.enqueue_read(0, 8).get(), np.float64)[0] for r in self.R))
         return float(np.frombuffer(self.R[0].enqueue_read(0, 8).get(), np.float64)[0])
 
 
-def dot_multi(devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None) -> float:
-    shards = DotShards(devices, a, b, comm)
+def dot_multi(devices: Sequence[DeviceHandle], a: np.ndarray, b: np.ndarray, comm=None,
+              fused: Optional[bool] = None) -> float:
+    shards = DotShards(devices, a, b, comm, fused)
     shards.enqueue()
     return shards.result()

@@ -108,3 +108,49 @@ class Communicator:
 def destroy(comm: Optional[Communicator]) -> None:
     if comm is not None:
         comm.close()
+
+
+class PeerGroup:
+    """Exchange blocks for reductions fused into kernels across the devices
+    this process drives (``ofl_dot_f32_allreduce``): one small zero-filled
+    block per device, written by every member over NVLink peer stores.  The
+    round counter orders successive reductions on the group (double-buffered
+    slots, monotonically increasing arrival counters, no resets)."""
+
+    def __init__(self, rt, devices: Sequence):
+        lib = _native.load()
+        if not 1 <= len(devices) <= 16:
+            raise BadArgsError("a peer group has 1..16 members")
+        nbytes = lib.ofl_xchg_bytes()
+        self._rt = rt
+        self.devices = list(devices)
+        self.blocks = [d.create_buffer(nbytes).get() for d in self.devices]
+        objs = [rt.local._buffer(b.gid) for b in self.blocks]
+        G = len(objs)
+        self.ptrs = (ctypes.c_void_p * G)(*[o.ptr for o in objs])
+        self.ordinals = (ctypes.c_int * G)(*[o.device.ordinal for o in objs])
+        self.round = 0
+
+    def dot_f32(self, a_bufs: Sequence, b_bufs: Sequence, out_bufs: Sequence,
+                counts: Sequence[int]) -> CompletionToken:
+        """Per-member fp32 dot of its shard, summed across the group inside
+        the kernels; every out buffer's first f64 holds the identical total."""
+        G = len(self.devices)
+        if not (len(a_bufs) == len(b_bufs) == len(out_bufs) == len(counts) == G):
+            raise BadArgsError("one shard per group member")
+        lib = _native.load()
+        local = self._rt.local
+        toks = []
+        ticket = ctypes.c_uint64()
+        for g in range(G):
+            A, B, R = (local._buffer(x.gid) for x in (a_bufs[g], b_bufs[g], out_bufs[g]))
+            n = int(counts[g])
+            if n > min(A.elements("buffer_f32"), B.elements("buffer_f32")) or R.size_bytes < 8:
+                raise BadArgsError("shard larger than its buffers")
+            st = A.device.stream(0)
+            _native.check(lib.ofl_dot_f32_allreduce(
+                st.ptr, A.ptr, B.ptr, R.ptr, n, g, G, self.ptrs, self.ordinals, self.round,
+                ctypes.byref(ticket)), "fused dot allreduce")
+            toks.append(st.token(ticket.value))
+        self.round += 1
+        return when_all(toks)

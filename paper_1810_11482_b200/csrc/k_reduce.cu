@@ -110,10 +110,55 @@ __global__ void __launch_bounds__(kThreads) k_sum_u32(const uint32_t* __restrict
   if (fold<uint32_t>(sc, acc, &total)) res[0] = total;
 }
 
+// Exchange block of one rank for the fused dot + allreduce (ofl_dot_f32_allreduce),
+// in that rank's device memory and written by every rank over NVLink.
+struct Xchg {
+  unsigned long long arrivals;  // monotonically counts partials received
+  unsigned long long status;    // non-zero: a rank gave up waiting (timeout)
+  double slot[2][OFL_MAX_PEER_RANKS];  // [round parity][rank]
+};
+
+struct PeerReduce {
+  Xchg* peers[OFL_MAX_PEER_RANKS];  // every rank's block (peer pointers)
+  int rank, nranks;
+  unsigned long long round;  // 0, 1, 2, ... per call on this group
+};
+
+// Last CTA of rank `rank`: publish the partial to every rank, then wait for
+// all partials of this round and sum them in rank order (identical bits on
+// every rank).  Bounded wait: after ~20 s the rank records a timeout.
+__device__ void peer_allreduce(const PeerReduce& pr, double partial, double* res) {
+  const int par = (int)(pr.round & 1);
+  for (int r = 0; r < pr.nranks; ++r)
+    *reinterpret_cast<volatile double*>(&pr.peers[r]->slot[par][pr.rank]) = partial;
+  __threadfence_system();
+  for (int r = 0; r < pr.nranks; ++r) atomicAdd_system(&pr.peers[r]->arrivals, 1ull);
+  Xchg* mine = pr.peers[pr.rank];
+  const unsigned long long target = (pr.round + 1) * (unsigned long long)pr.nranks;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*reinterpret_cast<volatile unsigned long long*>(&mine->arrivals) < target) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20ull * 1000 * 1000 * 1000) {
+      mine->status = 1;
+      res[0] = __longlong_as_double(0x7ff8000000000000ll);
+      return;
+    }
+    __nanosleep(200);
+  }
+  __threadfence_system();
+  double total = 0.0;
+  for (int r = 0; r < pr.nranks; ++r)
+    total += *reinterpret_cast<volatile double*>(&mine->slot[par][r]);
+  res[0] = total;
+}
+
+template <bool kPeer = false>
 __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ a,
                                                       const float* __restrict__ b,
                                                       double* __restrict__ res, uint64_t n,
-                                                      Scratch* sc) {
+                                                      Scratch* sc, PeerReduce pr = PeerReduce{}) {
   const uint64_t n4 = n >> 2;
   const float4* a4 = reinterpret_cast<const float4*>(a);
   const float4* b4 = reinterpret_cast<const float4*>(b);
@@ -147,7 +192,10 @@ __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ 
   }
   acc = block_sum(acc);
   double total;
-  if (fold<double>(sc, acc, &total)) res[0] = total;
+  if (fold<double>(sc, acc, &total)) {
+    if (kPeer) peer_allreduce(pr, total, res);
+    else res[0] = total;
+  }
 }
 
 // Grid: persistent, `cps` CTAs of 512 threads per SM with a grid-stride
@@ -209,6 +257,38 @@ extern "C" int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double
   k_dot_f32<<<blocks, kThreads, 0, s->cs>>>(a, b, res, n, reduce_scratch(scratch));
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return ofl::cuda_error(e, "dot launch");
+  ofl::count_launch();
+  return q.finish(ticket);
+}
+
+extern "C" int ofl_xchg_bytes(void) { return (int)sizeof(Xchg); }
+
+extern "C" int ofl_dot_f32_allreduce(ofl_stream* s, const float* a, const float* b, double* res,
+                                     uint64_t n, int rank, int nranks, void* const* xchg,
+                                     const int* devs, uint64_t round, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "dot operands must be 16-byte aligned");
+  if (nranks < 1 || nranks > OFL_MAX_PEER_RANKS || rank < 0 || rank >= nranks)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "dot allreduce: bad rank / group size");
+  PeerReduce pr{};
+  for (int r = 0; r < nranks; ++r) {
+    if (!xchg[r]) return ofl::set_error(OFL_ERR_BAD_ARGS, "dot allreduce: missing exchange block");
+    pr.peers[r] = static_cast<Xchg*>(xchg[r]);
+    if (devs[r] != s->dev) ofl::enable_peer(s->dev, devs[r]);
+  }
+  pr.rank = rank;
+  pr.nranks = nranks;
+  pr.round = round;
+  ofl::Enqueue q(s);
+  if (!q.ok()) return q.status;
+  const int blocks = grid_for(s, n >> 2, 2, kDotCtasPerSm);
+  void* scratch = nullptr;
+  int st = ofl::stream_scratch(s, scratch_bytes(blocks), &scratch);
+  if (st) return st;
+  k_dot_f32<true><<<blocks, kThreads, 0, s->cs>>>(a, b, res, n, reduce_scratch(scratch), pr);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return ofl::cuda_error(e, "dot allreduce launch");
   ofl::count_launch();
   return q.finish(ticket);
 }

@@ -51,6 +51,8 @@ int ofl_heat(void* s, void* x, void* y, uint64_t n, uint64_t k, int tb, uint64_t
 int ofl_heat_slab(void* s, const void* x, void* y, uint64_t n, int k, uint64_t lo, uint64_t hi, void* l, int ld, void* r, int rd, uint64_t h, uint64_t* t) { (void)x; (void)y; (void)n; (void)k; (void)lo; (void)hi; (void)l; (void)ld; (void)r; (void)rd; (void)h; launches++; return op(s, t); }
 int ofl_stencil2d(void* s, const void* x, void* y, uint32_t w, uint32_t h, uint64_t m, uint64_t lx, uint64_t* t) { (void)x; (void)y; (void)w; (void)h; (void)m; (void)lx; launches++; return op(s, t); }
 int ofl_stencil2d_slab(void* s, const void* x, void* y, uint32_t w, uint32_t h, uint32_t lo, uint32_t hi, void* u, int ud, void* d, int dd, uint64_t* t) { (void)x; (void)y; (void)w; (void)h; (void)lo; (void)hi; (void)u; (void)ud; (void)d; (void)dd; launches++; return op(s, t); }
+int ofl_xchg_bytes(void) { return 272; }
+int ofl_dot_f32_allreduce(void* s, const void* a, const void* b, void* r, uint64_t n, int rk, int nr, void* const* x, const int* d, uint64_t rd, uint64_t* t) { (void)a; (void)b; (void)r; (void)n; (void)rk; (void)nr; (void)x; (void)d; (void)rd; launches++; return op(s, t); }
 int ofl_mandelbrot(void* s, void* o, uint32_t w, uint32_t h, double a, double b, double c, double d, double e, uint32_t mi, uint64_t it, uint32_t rf, uint32_t rs, int cp, uint64_t* t) {
   (void)o; (void)w; (void)h; (void)a; (void)b; (void)c; (void)d; (void)e; (void)mi; (void)it; (void)rf; (void)rs; (void)cp; launches++; return op(s, t); }
 int ofl_sum_u32(void* s, const void* i, void* r, uint64_t n, uint64_t* t) { (void)i; (void)r; (void)n; launches++; return op(s, t); }

@@ -120,9 +120,32 @@ def test_dot_two_logical_devices_host_sum(rt2):
     devices = rt2.get_all_devices().get()
     a = np.random.default_rng(3).random(3_000_001, dtype=np.float32)
     b = np.random.default_rng(4).random(3_000_001, dtype=np.float32)
-    got = dot_multi(devices, a, b)  # no NCCL across logical devices of one GPU
+    got = dot_multi(devices, a, b, fused=False)  # partials summed on the host
     exp = oracle.dot_f32(a, b)
     assert abs(got - exp) <= 1e-12 * abs(exp)
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 5])
+def test_dot_fused_peer_allreduce(parts):
+    """Dot product with the cross-device sum fused into the reduction kernel
+    (peer-memory exchange, rank-order sum): every device holds the same
+    bits, within 1e-12 of the oracle; repeated rounds reuse the exchange
+    blocks (parity slots, monotonic counters)."""
+    from paper_1810_11482_b200.bench.harness import DotShards
+
+    import oracle
+
+    rng = np.random.default_rng(parts)
+    a = rng.random(1_000_003 * parts, dtype=np.float32)
+    b = rng.random(1_000_003 * parts, dtype=np.float32)
+    exp = oracle.dot_f32(a, b, threads=0)
+    with Runtime(devices=[0] * parts) as rt:
+        shards = DotShards(rt.get_all_devices().get(), a, b, fused=True)
+        for _ in range(5):
+            shards.enqueue().get(timeout=60)
+            vals = [np.frombuffer(r.enqueue_read(0, 8).get(), np.float64)[0] for r in shards.R]
+            assert len(set(v.tobytes() for v in vals)) == 1
+            assert abs(vals[0] - exp) <= 1e-12 * abs(exp)
 
 
 FAULT_SCRIPT = r"""
