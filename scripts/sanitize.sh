@@ -7,6 +7,6 @@ CS="compute-sanitizer --error-exitcode 9 --print-limit 20"
 W='import __graft_entry__ as g; g.smoke(); import sys; sys.argv=["x","--small"]; exec(open("scripts/sanitize_workloads.py").read())'
 for tool in memcheck racecheck synccheck initcheck; do
   echo "== $tool"
-  timeout 900 $CS --tool $tool python -c "$W" 2>&1 | grep -v "^smoke ok" | tail -6
+  timeout 900 $CS --tool $tool python -c "$W" 2>&1 | grep -v "^smoke ok" | tail -8
   echo "exit=${PIPESTATUS[0]}"
 done

@@ -45,4 +45,26 @@ with Runtime(devices=[0]) as rt:
     jp = d.create_program_with_source(src).get()
     jp.build("inc").get()
     jp.run([U, n], "inc", *g).get()
+    # 2-D stencil (row batch + per-cell kernels)
+    w2, h2 = 130, 67
+    S2a, S2b = d.create_buffer(w2 * h2 * 8).get(), d.create_buffer(w2 * h2 * 8).get()
+    S2a.enqueue_write(0, rng.random(w2 * h2))
+    p2 = d.create_program_with_source(kernel_source("stencil2d")).get()
+    p2.build("stencil2d").get()
+    p2.run([S2a, S2b, w2, h2], "stencil2d", (64, 1, 1), (256, 1, 1)).get()
+    p2.run([S2a, S2b, w2 - 1, h2], "stencil2d", (64, 1, 1), (256, 1, 1)).get()
     print("workloads ok")
+
+# multi-device paths with peer stores / peer atomics (logical devices)
+from paper_1810_11482_b200.bench.harness import DotShards, heat2d_multi, heat_multi  # noqa: E402
+
+with Runtime(devices=[0, 0, 0]) as rt3:
+    devs = rt3.get_all_devices().get()
+    rng = np.random.default_rng(9)
+    heat_multi(devs, rng.random(30_001), 70, halo=16, fused=True)
+    heat2d_multi(devs, rng.random(66 * 40), 66, 40, 5)
+    sh = DotShards(devs, rng.random(90_001, dtype=np.float32), rng.random(90_001, dtype=np.float32),
+                   fused=True)
+    sh.enqueue().get(timeout=60)
+    sh.enqueue().get(timeout=60)
+    print("multi-device ok")
