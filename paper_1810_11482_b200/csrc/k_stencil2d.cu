@@ -110,12 +110,16 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_march(const double* __re
 // loads (and the strip-edge loads) up front — RB + 2 independent 512-byte
 // requests per warp in flight — then computes and stores the RB rows.  The
 // two halo rows per strip mostly hit L2 (the neighbouring strips load them).
-template <int RB, bool kSlab = false>
+template <int RB, bool kSlab = false, bool kPDL = false>
 __global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __restrict__ x,
                                                               double* __restrict__ y, uint32_t w,
                                                               uint32_t h, uint64_t m, uint64_t lx,
                                                               uint32_t col_chunks,
                                                               SlabRows sr = SlabRows{}) {
+  if constexpr (kPDL) {  // programmatic dependent launch (see k_stream.cu)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const int lane = threadIdx.x & 31;
   const uint64_t wid = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const uint64_t cx = wid % col_chunks, ry = wid / col_chunks;
@@ -315,6 +319,23 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_cells(const double* __re
   }
 }
 
+// Launch with programmatic stream serialization: the kernel's CTAs may be
+// scheduled while the previous kernel on the stream drains; they wait in
+// griddepcontrol.wait before touching memory.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), unsigned blocks, cudaStream_t cs, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = cs;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // OFL_STENCIL2D_VARIANT (sweeps): 0 = batch of 8 rows per warp (default,
 // profiles/r01_stencil2d_sweep.txt), 1 = row marching (32 rows), 2/3/4 =
 // batch of 16/4/12 rows, 5 = TMA-staged tiles (4 stages; full grids)
@@ -359,7 +380,8 @@ extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t
       else if (v == 4)
         k_stencil2d_batch<12><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
       else
-        k_stencil2d_batch<8><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
+        launch_pdl(k_stencil2d_batch<8, false, true>, blocks, cs, x, y, w, h, m, x_elems,
+                   col_chunks, SlabRows{});
     } else {
       const uint64_t blocks = (m + kThreads - 1) / kThreads;
       k_stencil2d_cells<<<(unsigned)blocks, kThreads, 0, s->cs>>>(x, y, w, h, m);
