@@ -371,10 +371,48 @@ __device__ __forceinline__ void ghost_exchange(double (&c)[R], double (*sl)[K], 
   }
 }
 
+// tb steps of the two-level scheme: K barrier-free warp steps, then a ghost
+// refresh from the neighbouring warps; returns whether the state is in a.
+template <int R, int K, bool kFma, bool kEdge>
+__device__ __forceinline__ bool hier_steps(double (&a)[R], double (&b)[R], int lane, int warp,
+                                           int64_t g0, int64_t nn, int tb,
+                                           double (*sh_l)[kHierWarps][K],
+                                           double (*sh_r)[kHierWarps][K]) {
+  int s = 0, ex = 0;
+  bool in_a = true;
+  while (s < tb) {
+    int k = 0;
+    for (; k + 1 < K && s + k + 1 < tb; k += 2) {
+      if (in_a) {
+        warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
+        warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
+      } else {
+        warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
+        warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
+      }
+    }
+    if (k < K && s + k < tb) {
+      if (in_a) warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
+      else warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
+      in_a = !in_a;
+      ++k;
+    }
+    s += k;
+    if (s >= tb) break;
+    const int p = ex & 1;
+    ++ex;
+    if (in_a)
+      ghost_exchange<R, K>(a, sh_l[p], sh_r[p], lane, warp);
+    else
+      ghost_exchange<R, K>(b, sh_l[p], sh_r[p], lane, warp);
+  }
+  return in_a;
+}
+
 template <int R, int K>
 __global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __restrict__ x,
                                                                double* __restrict__ y,
-                                                               uint64_t n, int tb) {
+                                                               uint64_t n, int tb, bool fma_ok) {
   static_assert(2 * K <= R, "ghosts must fit in the edge lanes");
   constexpr int kOwn = 32 * R - 2 * K;        // owned cells per warp
   constexpr int kSpan = kHierWarps * kOwn;    // owned cells per CTA (incl. CTA halo)
@@ -390,36 +428,27 @@ __global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __r
     const int64_t g = g0 + i;
     a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
   }
-  int s = 0, ex = 0;
-  bool in_a = true;
-  while (s < tb) {
-    // K steps (or what is left) without any barrier
-    int k = 0;
-    for (; k + 1 < K && s + k + 1 < tb; k += 2) {
-      if (in_a) {
-        warp_step<R, false, true, true>(a, b, lane, g0, nn);
-        warp_step<R, false, true, true>(b, a, lane, g0, nn);
-      } else {
-        warp_step<R, false, true, true>(b, a, lane, g0, nn);
-        warp_step<R, false, true, true>(a, b, lane, g0, nn);
-      }
+  // CTA-uniform update form: ghosts carry neighbouring warps' values into a
+  // warp's tile, so the fused update's guard (warp_tile_steps) must hold for
+  // the whole CTA tile; the endpoint fix-up is likewise decided per CTA
+  bool safe = fma_ok;
+  if (safe) {
+    const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
+      safe &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
     }
-    if (k < K && s + k < tb) {
-      if (in_a) warp_step<R, false, true, true>(a, b, lane, g0, nn);
-      else warp_step<R, false, true, true>(b, a, lane, g0, nn);
-      in_a = !in_a;
-      ++k;
-    }
-    s += k;
-    if (s >= tb) break;
-    // ghost refresh from the neighbouring warps
-    const int p = ex & 1;
-    ++ex;
-    if (in_a)
-      ghost_exchange<R, K>(a, sh_l[p], sh_r[p], lane, warp);
-    else
-      ghost_exchange<R, K>(b, sh_l[p], sh_r[p], lane, warp);
   }
+  safe = __syncthreads_and(safe);
+  const bool edge = __syncthreads_or((g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1));
+  bool in_a;
+  if (safe)
+    in_a = edge ? hier_steps<R, K, true, true>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r)
+                : hier_steps<R, K, true, false>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r);
+  else
+    in_a = edge ? hier_steps<R, K, false, true>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r)
+                : hier_steps<R, K, false, false>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r);
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int own = warp * kOwn - K + lane * R + i;  // CTA owned coordinate
@@ -517,11 +546,15 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
       const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
       k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
     } else if (heat_kernel() == 3) {
-      constexpr int R = 16, K = 8;
-      const uint64_t span = (uint64_t)kHierWarps * (32 * R - 2 * K);
+      const int r = heat_cells_per_thread();
+      constexpr int K = 8;
+      const uint64_t span = (uint64_t)kHierWarps * (32 * (uint64_t)r - 2 * K);
       const uint64_t valid = span - 2 * (uint64_t)k;
       const unsigned blocks = (unsigned)((n + valid - 1) / valid);
-      k_heat_hier<R, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k);
+      if (r == 24)
+        k_heat_hier<24, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k, heat_fused());
+      else
+        k_heat_hier<16, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k, heat_fused());
     } else if (heat_kernel() == 2) {
       const int r = heat_cells_per_thread();
       const bool fma = heat_fused();
