@@ -92,6 +92,12 @@ int ofl_host_free(void* hptr);
 int ofl_h2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
 int ofl_d2h(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
 int ofl_d2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket);
+/* `rows` consecutive device rows of row_bytes each -> host rows dst_pitch
+ * apart (cudaMemcpy2DAsync): a device's packed rows land directly at their
+ * place in a strided host image (config 3's cyclic-row assembly; the
+ * reference assembles through bytes, harness.py:393-437). */
+int ofl_d2h_rows(ofl_stream* s, void* dst, uint64_t dst_pitch, const void* src,
+                 uint64_t row_bytes, uint64_t rows, uint64_t* ticket);
 /* H2D from pageable memory through a ring of pinned staging slots, the host
  * copy of one chunk overlapping the DMA of the previous one; returns once the
  * source has been fully staged (it may then be reused).  One ticket. */

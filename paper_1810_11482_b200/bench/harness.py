@@ -346,53 +346,59 @@ def run_mandelbrot_series(sizes: Sequence[int], device: DeviceHandle,
 class MandelbrotTiles:
     """Config 3 on several devices: rows r with r mod G == g go to device g
     (cyclic split — contiguous bands leave devices idle); each
-    device packs its rows densely and reads them into a pinned host block;
-    the host scatters a device's rows into the image as soon as that
-    device's read completes, while the others are still computing."""
+    device computes its rows packed densely.  A device's rows are computed in
+    ``chunks`` launches that alternate between two streams, and each chunk
+    is read with one strided DMA straight to its rows of the pinned host
+    image (``enqueue_read_rows_into``), so the read of chunk c overlaps the
+    computation of chunk c+1 and no host-side scatter copy is needed."""
 
     def __init__(self, devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
-                 viewport=VIEWPORT, esc: float = 4.0, stream: int = 0):
+                 viewport=VIEWPORT, esc: float = 4.0, stream: int = 0, chunks: int = 1):
         self.devices = list(devices)
         self.width, self.height, self.max_iter = width, height, max_iter
-        self.viewport, self.esc, self.stream = viewport, esc, stream
+        self.viewport, self.esc = viewport, esc
         G = len(self.devices)
         self.rows = [len(decomp.cyclic_rows(height, G, g)) for g in range(G)]
-        self.bufs = [d.create_buffer(max(4, r * width * 4)).get() for d, r in zip(self.devices, self.rows)]
         self.progs = [_builtin(d, "mandelbrot_rows") for d in self.devices]
-        self.hosts = [pinned_empty(max(1, r * width) * 4, np.uint32) for r in self.rows]
+        self.streams, self.parts = [], []
+        for g, d in enumerate(self.devices):
+            r = self.rows[g]
+            c = max(1, min(chunks, r))
+            self.streams.append([stream] if c == 1 else [d.create_stream(), d.create_stream()])
+            bounds = [r * i // c for i in range(c + 1)]
+            self.parts.append([(k0, k1, d.create_buffer(max(4, (k1 - k0) * width * 4)).get())
+                               for k0, k1 in zip(bounds, bounds[1:]) if k1 > k0])
+        self.image = pinned_empty(width * height * 4, np.uint32)
 
     def enqueue(self) -> list:
+        """Launch every chunk and its read into ``self.image``; returns the
+        read tokens."""
         G = len(self.devices)
         re0, re1, im0, im1 = self.viewport
+        w = self.width
         toks = []
         for g in range(G):
-            if self.rows[g] == 0:
-                toks.append(None)
-                continue
-            self.progs[g].run([self.bufs[g], self.width, self.height, re0, re1, im0, im1, self.esc,
-                               self.max_iter, g, G], "mandelbrot_rows", (1, 1, 1), (1, 1, 1),
-                              self.stream)
-            toks.append(self.bufs[g].enqueue_read_into(0, self.hosts[g], self.stream))
+            for i, (k0, k1, buf) in enumerate(self.parts[g]):
+                st = self.streams[g][i % len(self.streams[g])]
+                items = (g + (k1 - 1) * G + 1) * w  # through the chunk's last row
+                self.progs[g].run([buf, w, self.height, re0, re1, im0, im1, self.esc,
+                                   self.max_iter, g + k0 * G, G], "mandelbrot_rows",
+                                  (math.ceil(items / 256), 1, 1), (256, 1, 1), st)
+                toks.append(buf.enqueue_read_rows_into(0, self.image, w * 4, k1 - k0,
+                                                       (g + k0 * G) * w * 4, G * w * 4, st))
         return toks
 
-    def assemble(self, toks: list, image: np.ndarray) -> np.ndarray:
-        G = len(self.devices)
-        img = image.reshape(self.height, self.width)
-        for g, t in enumerate(toks):
-            if t is None:
-                continue
-            t.get()
-            img[g::G] = self.hosts[g][: self.rows[g] * self.width].reshape(-1, self.width)
-        return image
-
     def __call__(self, image: Optional[np.ndarray] = None) -> np.ndarray:
-        image = image if image is not None else np.empty(self.width * self.height, np.uint32)
-        return self.assemble(self.enqueue(), image)
+        when_all(self.enqueue()).get()
+        if image is None:
+            return np.array(self.image)
+        image[:] = self.image
+        return image
 
 
 def mandelbrot_multi(devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
-                     viewport=VIEWPORT, esc: float = 4.0) -> np.ndarray:
-    return MandelbrotTiles(devices, width, height, max_iter, viewport, esc)()
+                     viewport=VIEWPORT, esc: float = 4.0, chunks: int = 1) -> np.ndarray:
+    return MandelbrotTiles(devices, width, height, max_iter, viewport, esc, chunks=chunks)()
 
 
 # -- heat equation across devices (config 2) ---------------------------------------

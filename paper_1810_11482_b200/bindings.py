@@ -281,12 +281,21 @@ def _heat_launch(st, v, items, ticket):
     return st.lib.ofl_heat(st.ptr, x.ptr, y.ptr, n, steps, heat_block(), ticket)
 
 
-def _rows_oob(v, items):
-    out, width, height = v[0], v[1], v[2]
+def _rows_exec(v, items) -> int:
+    """Rows a mandelbrot_rows launch computes: row_first + k*row_step below
+    the image height and holding a pixel gtid < min(items, width*height)."""
+    width, height = v[1], v[2]
     row_first, row_step = v[9], v[10]
-    rows = 0 if row_first >= height or row_step == 0 else (height - row_first + row_step - 1) // row_step
-    need = rows * width
-    lo = out.elements("buffer_u32")
+    limit = min(items, (width * height) & M32)
+    if limit == 0 or width == 0 or row_step == 0 or row_first >= height:
+        return 0
+    last = min(height - 1, (limit - 1) // width)
+    return 0 if last < row_first else (last - row_first) // row_step + 1
+
+
+def _rows_oob(v, items):
+    need = _rows_exec(v, items) * v[1]
+    lo = v[0].elements("buffer_u32")
     return lo if need > lo else None
 
 
@@ -296,7 +305,7 @@ def _rows_launch(st, v, items, ticket):
         raise BadArgsError("mandelbrot_rows: row_step must be >= 1")
     return st.lib.ofl_mandelbrot(
         st.ptr, out.ptr, width, height, float(re0), float(re1), float(im0), float(im1),
-        float(esc), max_iter, (width * height) & M32, row_first, row_step, 1, ticket,
+        float(esc), max_iter, min(items, (width * height) & M32), row_first, row_step, 1, ticket,
     )
 
 
@@ -311,7 +320,8 @@ BUILTIN_KERNELS = {
         "heat", ("buffer_f64", "buffer_f64", "scalar_u32", "scalar_u32"), _heat_launch, _heat_oob
     ),
     # mandelbrot.k over rows row_first + k*row_step only, packed densely
-    # (multi-GPU cyclic row split; the launch shape is ignored)
+    # (multi-GPU cyclic row split); as in mandelbrot.k only pixels
+    # gtid < min(grid*block, width*height) are computed
     "mandelbrot_rows": Binding(
         "mandelbrot_rows",
         ("buffer_u32", "scalar_u32", "scalar_u32", "scalar_f64", "scalar_f64", "scalar_f64",

@@ -134,6 +134,31 @@ class BufferObject:
         return DeviceToken(st, ticket.value, lambda: (landing.take(), out)[1])
 
 
+    def enqueue_read_rows_into(self, offset: int, out, row_bytes: int, rows: int,
+                               dst_offset: int, dst_pitch: int, stream: int = 0):
+        """Copy `rows` consecutive rows of `row_bytes` starting at `offset`
+        into the pinned host buffer `out`, row i at byte dst_offset +
+        i*dst_pitch (one strided DMA; cudaMemcpy2DAsync).  Token value: out."""
+        addr, n, owner = hostmem.writable_view(out)
+        span = rows * row_bytes
+        check_range(offset, span, self.size_bytes, "read")
+        if rows and (dst_pitch < row_bytes or dst_offset < 0
+                     or dst_offset + (rows - 1) * dst_pitch + row_bytes > n):
+            raise BadArgsError("row read does not fit the destination")
+        if span == 0:
+            return make_ready(out)
+        if not hostmem.is_pinned(addr, n):
+            raise BadArgsError("enqueue_read_rows_into needs a pinned destination (pinned_empty)")
+        st = self.device.stream(stream)
+        ticket = ctypes.c_uint64()
+        status = st.lib.ofl_d2h_rows(st.ptr, addr + dst_offset, dst_pitch, self.ptr + offset,
+                                     row_bytes, rows, ctypes.byref(ticket))
+        if status:
+            raise_status(status, "read")
+        st.keep(ticket.value, owner)
+        return DeviceToken(st, ticket.value, lambda: out)
+
+
 class _Landing:
     """A staging block receiving a device->host copy.  `take` (after
     completion) extracts the data; the block is recycled once both the copy

@@ -357,6 +357,19 @@ int ofl_h2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t*
 int ofl_d2h(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket) {
   return copy_op(s, dst, src, bytes, cudaMemcpyDeviceToHost, ticket);
 }
+int ofl_d2h_rows(ofl_stream* s, void* dst, uint64_t dst_pitch, const void* src,
+                 uint64_t row_bytes, uint64_t rows, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (dst_pitch < row_bytes) return set_error(OFL_ERR_BAD_ARGS, "destination pitch < row bytes");
+  Enqueue q(s);
+  if (!q.ok()) return q.status;
+  if (row_bytes && rows) {
+    cudaError_t e = cudaMemcpy2DAsync(dst, dst_pitch, src, row_bytes, row_bytes, rows,
+                                      cudaMemcpyDeviceToHost, s->cs);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpy2DAsync");
+  }
+  return q.finish(ticket);
+}
 int ofl_d2d(ofl_stream* s, void* dst, const void* src, uint64_t bytes, uint64_t* ticket) {
   return copy_op(s, dst, src, bytes, cudaMemcpyDeviceToDevice, ticket);
 }

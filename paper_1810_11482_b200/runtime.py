@@ -112,6 +112,16 @@ class CudaDispatch:
         except Exception as exc:  # noqa: BLE001
             return make_failed(exc)
 
+    def read_rows_into(self, buffer_gid, offset, out, row_bytes, rows, dst_offset, dst_pitch,
+                       stream, device=None) -> CompletionToken:
+        try:
+            buf = self._buffer(buffer_gid)
+            return self._traced(buf.device, stream, "read", rows * row_bytes,
+                                lambda: buf.enqueue_read_rows_into(offset, out, row_bytes, rows,
+                                                                   dst_offset, dst_pitch, stream))
+        except Exception as exc:  # noqa: BLE001
+            return make_failed(exc)
+
     def read_into(self, buffer_gid, offset, out, stream, device=None) -> CompletionToken:
         try:
             buf = self._buffer(buffer_gid)

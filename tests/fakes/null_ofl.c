@@ -73,5 +73,6 @@ int ofl_jit_compile(int d, const char* s, const char* e, void** o, char* l, int 
 int ofl_jit_launch(void* s, void* k, void** p, uint64_t b, int t, uint64_t* tk) { (void)k; (void)p; (void)b; (void)t; return op(s, tk); }
 int ofl_jit_destroy(void* k) { (void)k; return 0; }
 int ofl_fill_ones(void* s, void* d, uint64_t n, uint64_t* t) { memset(d, 0xff, n); return op(s, t); }
+int ofl_d2h_rows(void* s, void* d, uint64_t dp, const void* x, uint64_t rb, uint64_t r, uint64_t* t) { for (uint64_t i = 0; i < r; ++i) memcpy((char*)d + i * dp, (const char*)x + i * rb, rb); return op(s, t); }
 int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
 int ofl_host_memcpy(void* d, const void* s, uint64_t n) { memcpy(d, s, n); return 0; }

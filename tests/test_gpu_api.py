@@ -171,6 +171,29 @@ def test_pinned_zero_copy_roundtrip(dev):
     assert np.array_equal(src, dst)
 
 
+def test_read_rows_into_strided_pinned(dev):
+    """Packed device rows land at a stride in a pinned host array (one DMA);
+    misuse raises synchronously."""
+    from paper_1810_11482_b200 import BadArgsError, OobAccessError, pinned_empty
+
+    rows, w = 7, 40
+    src = np.arange(rows * w, dtype=np.uint32)
+    buf = dev.create_buffer(src.nbytes).get()
+    buf.enqueue_write(0, src.tobytes())
+    img = pinned_empty(3 * rows * w * 4, np.uint32)
+    img[:] = 0xFFFFFFFF
+    buf.enqueue_read_rows_into(0, img, w * 4, rows, dst_offset=w * 4, dst_pitch=3 * w * 4).get()
+    exp = np.full((3 * rows, w), 0xFFFFFFFF, np.uint32)
+    exp[1::3] = src.reshape(rows, w)
+    assert np.array_equal(img.reshape(-1, w), exp)
+    with pytest.raises(OobAccessError):
+        buf.enqueue_read_rows_into(0, img, w * 4, rows + 1)
+    with pytest.raises(BadArgsError):
+        buf.enqueue_read_rows_into(0, img, w * 4, rows, dst_offset=0, dst_pitch=w * 4 - 4)
+    with pytest.raises(BadArgsError):
+        buf.enqueue_read_rows_into(0, np.empty(3 * rows * w, np.uint32), w * 4, rows)
+
+
 def test_read_into_pageable(dev):
     buf = dev.create_buffer(1024).get()
     buf.enqueue_write(0, bytes(range(256)) * 4)
@@ -428,8 +451,21 @@ def test_mandelbrot_cyclic_rows_two_devices(rt2):
     import oracle
 
     devices = rt2.get_all_devices().get()
-    counts = mandelbrot_multi(devices, 640, 360, 1000)
-    assert counts.tobytes() == oracle.mandelbrot(640, 360, max_iter=1000, threads=0).tobytes()
+    exp = oracle.mandelbrot(640, 360, max_iter=1000, threads=0).tobytes()
+    for chunks in (1, 3, 8, 500):
+        counts = mandelbrot_multi(devices, 640, 360, 1000, chunks=chunks)
+        assert counts.tobytes() == exp, chunks
+
+
+def test_mandelbrot_chunked_single_device_config3(dev, golden):
+    """Config 3 on one device in 8 chunks on two streams (read of chunk c
+    overlapping chunk c+1): the reference's sha256."""
+    import hashlib
+
+    from paper_1810_11482_b200.bench.harness import mandelbrot_multi
+
+    counts = mandelbrot_multi([dev], 7680, 4320, 2000, chunks=8)
+    assert hashlib.sha256(counts.tobytes()).hexdigest() == golden["mandelbrot"][7]["sha256"]
 
 
 def test_heat_multi_device_halo(rt2):
