@@ -25,6 +25,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTileW = 8, kTileH = 4;  // one warp
 constexpr int kTilesPerUnit = 4;       // 32x4 pixels per queue pop
+#ifndef OFL_PERIOD_CHECK
+#define OFL_PERIOD_CHECK 16
+#endif
+constexpr uint32_t kPeriodCheck = OFL_PERIOD_CHECK;  // cycle test every k iterations (power of 2)
 
 struct MandelArgs {
   uint32_t* out;
@@ -37,6 +41,7 @@ struct MandelArgs {
   uint64_t units;
   int compact;  // 1: row r of this launch lands at out[r*width + px]
   int fused;    // allow the FUSED iteration (escape_countP) under its guard
+  int period;   // exact cycle detection (escape_countP PERIOD)
 };
 
 // INTCMP: the escape test `mag > esc` done on the bit patterns (int64
@@ -111,20 +116,32 @@ __device__ __forceinline__ void escape_count2(double cra, double cia, double crb
 // when every pixel of the warp has |cre|, |cim| >= 2^-400: a sum of two
 // doubles one of which is >= 2^-400 is 0 or >= 2^-454 in magnitude, so zr
 // and zi stay in {0} U [2^-454, 1e5] and zr*zi in {0} U [2^-908, 1e10].
-template <bool INTCMP, int P, bool FUSED = false>
+//
+// PERIOD: exact cycle detection (Brent).  The iteration is a deterministic
+// map on the double pair (zr, zi); if the state after iteration i is bit-
+// for-bit the state saved after iteration s < i, the orbit repeats forever,
+// every value on the cycle already passed the escape test, so the pixel
+// never escapes: its count is max_iter — exactly what iterating to max_iter
+// gives.  States are saved at iterations 16, 32, 64, ... and compared every
+// 16th iteration (64-bit integer compares on the ALU pipe; every 4/8/16/32:
+// 2.98/2.71/2.68/2.97 ms for config 3, profiles/r01_mandel_sweep.txt).
+template <bool INTCMP, int P, bool FUSED = false, bool PERIOD = false>
 __device__ __forceinline__ void escape_countP(const double (&cr)[P], const double (&ci)[P],
                                               double esc, uint32_t max_iter, uint32_t (&n)[P]) {
   // zr^2 and zi^2 are carried from one iteration to the next (computed
   // right after the update) so each is evaluated once per iteration.
   double zr[P], zi[P], r2[P], i2[P];
+  long long sr[P], si[P];  // saved state (bit patterns) for PERIOD
   bool live[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     zr[p] = zi[p] = r2[p] = i2[p] = 0.0;
+    sr[p] = si[p] = 0x7ff8000000000001ll;  // matches no iterate
     n[p] = 0;
     live[p] = true;
   }
   const long long esc_bits = __double_as_longlong(esc);
+  uint32_t save_at = kPeriodCheck;
   for (uint32_t i = 0; i < max_iter; ++i) {
     bool any = false;
 #pragma unroll
@@ -149,6 +166,24 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
       r2[p] = __dmul_rn(zr[p], zr[p]);
       i2[p] = __dmul_rn(zi[p], zi[p]);
     }
+    if (PERIOD && (i & (kPeriodCheck - 1)) == kPeriodCheck - 1) {  // state after iteration i+1
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const long long zb = __double_as_longlong(zr[p]), wb = __double_as_longlong(zi[p]);
+        if (live[p] && zb == sr[p] && wb == si[p]) {
+          n[p] = max_iter;  // periodic: never escapes
+          live[p] = false;
+        }
+      }
+      if (i + 1 == save_at) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          sr[p] = __double_as_longlong(zr[p]);
+          si[p] = __double_as_longlong(zi[p]);
+        }
+        save_at <<= 1;
+      }
+    }
   }
 }
 
@@ -162,8 +197,11 @@ __device__ __forceinline__ bool fused_ok(const double (&cr)[P], const double (&c
 }
 
 // ILP-P variant: lane l handles the same position of the P tiles of a unit.
-template <bool INTCMP, int P>
-__global__ void __launch_bounds__(kThreads) k_mandelbrotP(MandelArgs a, unsigned int* queue) {
+// PERIOD keeps two more saved doubles per pixel; capping it at 3 CTAs/SM
+// (85 registers) keeps the occupancy of the plain kernel
+template <bool INTCMP, int P, bool PERIOD = false>
+__global__ void __launch_bounds__(kThreads, PERIOD ? 3 : 1) k_mandelbrotP(MandelArgs a,
+                                                                       unsigned int* queue) {
   static_assert(kTilesPerUnit % P == 0, "P must divide the unit");
   const int lane = threadIdx.x & 31;
   const double dre = __dsub_rn(a.re1, a.re0);
@@ -199,9 +237,9 @@ __global__ void __launch_bounds__(kThreads) k_mandelbrotP(MandelArgs a, unsigned
         ci[j] = ok[j] ? c_im : 1.0;
       }
       if (INTCMP && a.fused && fused_ok<P>(cr, ci))
-        escape_countP<INTCMP, P, true>(cr, ci, a.esc, a.max_iter, cnt);
+        escape_countP<INTCMP, P, true, PERIOD>(cr, ci, a.esc, a.max_iter, cnt);
       else
-        escape_countP<INTCMP, P, false>(cr, ci, a.esc, a.max_iter, cnt);
+        escape_countP<INTCMP, P, false, PERIOD>(cr, ci, a.esc, a.max_iter, cnt);
 #pragma unroll
       for (int j = 0; j < P; ++j)
         if (ok[j]) a.out[at[j]] = cnt[j];
@@ -316,6 +354,11 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       return e ? atoi(e) != 0 : 1;
     }();
     a.fused = fused;
+    static const int period = [] {  // OFL_MANDEL_PERIOD=0 disables (sweeps)
+      const char* e = getenv("OFL_MANDEL_PERIOD");
+      return e ? atoi(e) != 0 : 1;
+    }();
+    a.period = period;
     // rows of this launch that can hold a pixel with gtid < limit
     const uint64_t last_row = (limit - 1) / width;  // highest py needed
     const uint64_t max_py = last_row < (uint64_t)height - 1 ? last_row : (uint64_t)height - 1;
@@ -346,9 +389,15 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       }();
       if (ilp == 4) {
         if (intcmp)
-          k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+          if (a.period)
+            k_mandelbrotP<true, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+          else
+            k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
         else
-          k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+          if (a.period)
+            k_mandelbrotP<false, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+          else
+            k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       } else if (ilp == 3) {  // the generic template at P=2
         if (intcmp)
           k_mandelbrotP<true, 2><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
