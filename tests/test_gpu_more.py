@@ -255,3 +255,29 @@ def test_stencil2d_tma_variant_bitexact():
     r = subprocess.run([sys.executable, "-c", TMA2D_SCRIPT, repo], capture_output=True, text=True,
                        timeout=300, env=env)
     assert r.stdout.strip().endswith("tma ok"), r.stdout[-500:] + r.stderr[-1500:]
+
+
+PLAIN_MANDEL_SCRIPT = r"""
+import sys, hashlib, json
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from flows import device_mandelbrot
+from paper_1810_11482_b200 import Runtime
+golden = json.load(open(sys.argv[1] + "/tests/golden/golden.json"))
+with Runtime(devices=[0]) as rt:
+    dev = rt.get_all_devices().get()[0]
+    raw = device_mandelbrot(dev, 7680, 4320, 2000)
+    assert hashlib.sha256(raw).hexdigest() == golden["mandelbrot"][7]["sha256"]
+print("plain ok")
+"""
+
+
+def test_mandelbrot_plain_kernel_config3():
+    """The kernel without cycle detection (OFL_MANDEL_PERIOD=0, the FP64
+    roofline reference) still reproduces the reference's config-3 counts."""
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", PLAIN_MANDEL_SCRIPT, repo], capture_output=True,
+                       text=True, timeout=300, env=dict(os.environ, OFL_MANDEL_PERIOD="0"))
+    assert r.stdout.strip().endswith("plain ok"), r.stdout[-500:] + r.stderr[-1500:]
