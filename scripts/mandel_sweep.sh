@@ -1,3 +1,5 @@
-for v in "OFL_MANDEL_ILP=2" "OFL_MANDEL_ILP=4" "OFL_MANDEL_ILP=8"; do
-  echo "== $v"; env $v python scripts/bench_configs.py --only mandel 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin)['config3_mandelbrot']; print(d['kernel_ms'], d['frac_fp64'], d['sha256_matches_reference'], d['fp64_peak_measured_tops'])"
+# Mandelbrot (config 3) variants: pixels per thread in lock step (OFL_MANDEL_ILP 1/2/3/4),
+# exact cycle detection on/off (OFL_MANDEL_PERIOD), fused zi update on/off (OFL_MANDEL_FUSED).
+for v in "OFL_MANDEL_ILP=4" "OFL_MANDEL_ILP=2" "OFL_MANDEL_PERIOD=0" "OFL_MANDEL_PERIOD=0 OFL_MANDEL_FUSED=0"; do
+  echo "== $v"; env $v python scripts/probes/mandel_clock.py
 done
