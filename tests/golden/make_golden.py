@@ -183,7 +183,72 @@ def stencil2d_cases(dev) -> dict:
     return {"step": cases, "heat": heat}
 
 
+def fuzz_cases(dev, count: int = 150) -> list:
+    """Random well-typed kernels from the reference's own generator
+    (pkg/tests/kernelgen.py), run by the reference on ONE work item (no
+    write races, so a parallel executor must match bit for bit), with the
+    final buffer states and any abort.  sin/cos-free: glibc and CUDA libm may
+    differ in the last ulp, which integer casts can amplify."""
+    import random
+
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from kernelgen import random_kernel
+    from offloadrt.errors import OffloadError
+
+    rng = random.Random(0x1810)
+    cases = []
+    while len(cases) < count:
+        src = random_kernel(rng)
+        if "sin(" in src or "cos(" in src:
+            continue
+        prog = dev.create_program_with_source(src).get()
+        prog.build("fuzzed").get(timeout=600)
+        irs = __import__("offloadrt.kernel", fromlist=["parse_and_validate"]).parse_and_validate(src)
+        params = irs["fuzzed"].params
+        vr = np.random.default_rng(len(cases))
+        handles, inits, args = [], [], []
+        for _, kind in params:
+            if kind == "buffer_f64":
+                init = vr.uniform(-100.0, 100.0, size=24)
+            elif kind == "buffer_u32":
+                init = vr.integers(0, 2**32, size=24, dtype=np.uint32)
+            else:
+                init = None
+            if init is not None:
+                h = dev.create_buffer(init.nbytes).get()
+                h.enqueue_write(0, init.tobytes()).get()
+                handles.append(h)
+                inits.append(["buf", kind, init.tobytes().hex()])
+                args.append(h)
+            elif kind == "scalar_f64":
+                v = float(vr.uniform(-50.0, 50.0))
+                inits.append(["f64", kind, v])
+                args.append(v)
+            else:
+                v = int(vr.integers(0, 2**32))
+                inits.append(["u32", kind, v])
+                args.append(v)
+        err = None
+        try:
+            prog.run(args, "fuzzed", (1, 1, 1), (1, 1, 1)).get(timeout=600)
+        except OffloadError as exc:
+            err = [type(exc).__name__, str(exc)]
+        outs = [h.enqueue_read_sync(0, h.size_bytes).hex() for h in handles]
+        cases.append({"source": src, "args": inits, "outputs_hex": outs, "error": err})
+    return cases
+
+
 def main() -> None:
+    if "--only-fuzz" in sys.argv:  # add/refresh the fuzz section in place
+        path = os.path.join(HERE, "golden.json")
+        with open(path) as fh:
+            out = json.load(fh)
+        with Runtime(backend="host") as rt:
+            out["fuzz"] = fuzz_cases(rt.get_all_devices().get()[0])
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+        print(f"updated fuzz ({len(out['fuzz'])} kernels) in golden.json")
+        return
     if "--only-stencil2d" in sys.argv:  # add/refresh one section in place
         path = os.path.join(HERE, "golden.json")
         with open(path) as fh:
@@ -199,6 +264,7 @@ def main() -> None:
     with Runtime(backend="host") as rt:
         dev = rt.get_all_devices().get()[0]
         out["stencil2d"] = stencil2d_cases(dev)
+        out["fuzz"] = fuzz_cases(dev)
 
         # -- stencil: hand case + random sizes (test_acceptance.py:62-66) ----
         cases = []

@@ -74,3 +74,34 @@ def test_jit_smallest_failing_gtid_reported(dev):
     buf = dev.create_buffer(100 * 8).get()
     with pytest.raises(OobAccessError, match="kernel buffer index 102 out of range"):
         p.run([buf, 0], "o", (4, 1, 1), (256, 1, 1)).get()
+
+
+def test_fuzzed_kernels_match_reference(dev, golden):
+    """150 random well-typed kernels from the reference's own generator
+    (tests/golden/make_golden.py --only-fuzz), one work item each: the
+    NVRTC-compiled kernel reproduces the reference executor's final buffer
+    states bit for bit, and its abort (OOB index, division by zero, cast
+    range) with the same error type and message."""
+    failures = []
+    for i, case in enumerate(golden["fuzz"]):
+        prog = dev.create_program_with_source(case["source"]).get()
+        prog.build("fuzzed").get(timeout=120)
+        handles, args = [], []
+        for tag, kind, value in case["args"]:
+            if tag == "buf":
+                h = dev.create_buffer(len(bytes.fromhex(value))).get()
+                h.enqueue_write(0, bytes.fromhex(value))
+                handles.append(h)
+                args.append(h)
+            else:
+                args.append(value)
+        tok = prog.run(args, "fuzzed", (1, 1, 1), (1, 1, 1))
+        err = None
+        try:
+            tok.get(timeout=60)
+        except (InternalError, OobAccessError) as exc:
+            err = [type(exc).__name__, str(exc)]
+        outs = [h.enqueue_read_sync(0, h.size_bytes).hex() for h in handles]
+        if err != case["error"] or outs != case["outputs_hex"]:
+            failures.append((i, err, case["error"], case["source"]))
+    assert not failures, f"{len(failures)} of {len(golden['fuzz'])} differ; first: {failures[0]}"
