@@ -281,3 +281,35 @@ def test_mandelbrot_plain_kernel_config3():
     r = subprocess.run([sys.executable, "-c", PLAIN_MANDEL_SCRIPT, repo], capture_output=True,
                        text=True, timeout=300, env=dict(os.environ, OFL_MANDEL_PERIOD="0"))
     assert r.stdout.strip().endswith("plain ok"), r.stdout[-500:] + r.stderr[-1500:]
+
+
+def test_stream_fifo_random_schedules(dev):
+    """Reference test_acceptance.py:286-308 in spirit: random schedules of
+    writes and reads on one stream behave exactly like their sequential
+    application (every read sees the state at its position), over many
+    schedules, plus a second stream joined by synchronize()."""
+    rng = np.random.default_rng(2018)
+    size = 256
+    buf = dev.create_buffer(size).get()
+    s1 = dev.create_stream()
+    for schedule in range(200):
+        model = bytearray(size)
+        buf.enqueue_write(0, bytes(size)).get()
+        checks = []
+        for _ in range(int(rng.integers(5, 25))):
+            off = int(rng.integers(0, size))
+            n = int(rng.integers(0, size - off + 1))
+            if rng.random() < 0.6:
+                data = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+                buf.enqueue_write(off, data)
+                model[off:off + n] = data
+            else:
+                checks.append((buf.enqueue_read(off, n), bytes(model[off:off + n])))
+        for tok, want in checks:
+            assert tok.get(timeout=30) == want, schedule
+        # a write on another stream becomes visible after synchronize()
+        data = rng.integers(0, 256, 16, dtype=np.uint8).tobytes()
+        buf.enqueue_write(8, data, s1)
+        dev.synchronize().get(timeout=30)
+        model[8:24] = data
+        assert buf.enqueue_read(0, size).get(timeout=30) == bytes(model), schedule
