@@ -7,6 +7,8 @@ python scripts/bench_configs.py --out gpurun_out/configs.json > /dev/null 2> gpu
 N="ncu --set full --clock-control none --import-source on"
 $N -k regex:k_stream_tile -s 1 -c 1 -o gpurun_out/rp_triad python scripts/profile_kernels.py triad > gpurun_out/ncu_triad.log 2>&1
 $N -k regex:k_mandelbrotP -s 1 -c 1 -o gpurun_out/rp_mandel python scripts/profile_kernels.py mandel > gpurun_out/ncu_mandel.log 2>&1
+OFL_MANDEL_PERIOD=0 $N -k regex:k_mandelbrotP -s 1 -c 1 -o gpurun_out/rp_mandel_plain python scripts/profile_kernels.py mandel > gpurun_out/ncu_mandel_plain.log 2>&1
+$N -k regex:k_stencil2d -s 2 -c 1 -o gpurun_out/rp_stencil2d python scripts/bench_configs.py --only stencil2d > /dev/null 2>&1
 $N -k regex:k_heat_warp -s 1 -c 1 -o gpurun_out/rp_heat python scripts/profile_kernels.py heat > gpurun_out/ncu_heat.log 2>&1
 $N -k regex:k_dot -s 1 -c 1 -o gpurun_out/rp_dot python scripts/profile_kernels.py dot > gpurun_out/ncu_dot.log 2>&1
 $N -k regex:k_sum -s 1 -c 1 -o gpurun_out/rp_sum python scripts/profile_kernels.py sum > gpurun_out/ncu_sum.log 2>&1
