@@ -290,14 +290,15 @@ struct SlabOut {
   double* right;  // receives y[own_hi - h, own_hi), or null
 };
 
-// Four 128-thread CTAs per SM for R <= 24: caps registers at 128 (a few
-// bytes of spill outside the step loop) and lifts residency from 12 to 16
-// warps per SM, which hides the tile loads better (R=24 tb=64: 43.9 ms for
-// config 2 vs 45.2 at 3 CTAs/SM and 51.7 unconstrained at 209 registers).
+// Residency by tile size (profiles/r01_heat_sweep.txt): four 128-thread
+// CTAs per SM for R <= 24 (128 registers), three for R <= 30 (168), two
+// above.  Default R=30 at 3 CTAs/SM: 41.2 ms for config 2 (R=24 at 4 CTAs:
+// 43.9; 13% instead of 17% redundant halo cells outweighs the lower
+// residency); R=32 at 3 CTAs spills inside the step loop (50.0 ms).
 // The slab form (extra peer stores) would spill at 128, so it gets three.
 template <int R, bool kSlab>
 constexpr int heat_warp_min_blocks() {
-  return kSlab ? 3 : (R <= 24 ? 4 : 2);
+  return kSlab ? 3 : (R <= 24 ? 4 : (R <= 30 ? 3 : 2));
 }
 
 template <int R, bool kSlab = false>
@@ -490,14 +491,14 @@ static int heat_kernel() {
   return v;
 }
 
-// cells per thread of the register kernels (OFL_HEAT_R: 8, 16, 24, 32);
+// cells per thread of the register kernels (OFL_HEAT_R: 8, 16, 20, 24, 26, 28, 30, 32);
 // default per kernel from profiles/r01_heat_sweep.txt
 static int heat_cells_per_thread() {
   static int v = [] {
     const char* e = getenv("OFL_HEAT_R");
-    const int dflt = heat_kernel() == 2 ? 24 : 8;
+    const int dflt = heat_kernel() == 2 ? 30 : 8;
     const int r = e ? atoi(e) : dflt;
-    return (r == 8 || r == 16 || r == 24 || r == 32) ? r : dflt;
+    return (r == 8 || r == 16 || r == 20 || r == 24 || r == 26 || r == 28 || r == 30 || r == 32) ? r : dflt;
   }();
   return v;
 }
@@ -565,6 +566,14 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
         k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
       else if (r == 24)
         k_heat_warp<24><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
+      else if (r == 20)
+        k_heat_warp<20><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
+      else if (r == 28)
+        k_heat_warp<28><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
+      else if (r == 26)
+        k_heat_warp<26><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
+      else if (r == 30)
+        k_heat_warp<30><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
       else
         k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
     } else {
