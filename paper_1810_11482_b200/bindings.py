@@ -261,7 +261,7 @@ def _dot_launch(st, v, items, ticket):
 def heat_block() -> int:
     """Steps fused per HBM pass by the heat builtin (OFL_HEAT_TB, default 64 —
     the fastest measured schedule, profiles/r01_heat_sweep.txt)."""
-    return max(1, min(64, int(os.environ.get("OFL_HEAT_TB", "64"))))
+    return max(1, min(128, int(os.environ.get("OFL_HEAT_TB", "64"))))
 
 
 def _heat_oob(v, items):

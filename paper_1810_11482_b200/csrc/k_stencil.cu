@@ -517,7 +517,8 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
                         uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (n < 1) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat needs n >= 1");
-  if (tb < 1 || tb > 64) return ofl::set_error(OFL_ERR_BAD_ARGS, "temporal block must be 1..64");
+  if (tb < 1 || tb > 128) return ofl::set_error(OFL_ERR_BAD_ARGS, "temporal block must be 1..128");
+  if (heat_kernel() != 2 && tb > 64) tb = 64;  // the sweep kernels size their tiles for <= 64
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat operands must be 16-byte aligned");
   ofl::Enqueue q(s);
