@@ -142,7 +142,8 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
   }
   const long long esc_bits = __double_as_longlong(esc);
   uint32_t save_at = kPeriodCheck;
-  for (uint32_t i = 0; i < max_iter; ++i) {
+  // one iteration for every pixel; false once no pixel of the thread is live
+  auto iterate = [&]() -> bool {
     bool any = false;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -151,7 +152,7 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
       live[p] = live[p] && !out;
       any = any || live[p];
     }
-    if (!any) break;
+    if (!any) return false;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       // predicated increment (one instruction; the plain `n += live` form
@@ -166,8 +167,20 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
       r2[p] = __dmul_rn(zr[p], zr[p]);
       i2[p] = __dmul_rn(zi[p], zi[p]);
     }
-    if (PERIOD && (i & (kPeriodCheck - 1)) == kPeriodCheck - 1) {  // state after iteration i+1
-#pragma unroll
+    return true;
+  };
+  if constexpr (!PERIOD) {
+    for (uint32_t i = 0; i < max_iter; ++i)
+      if (!iterate()) return;
+  } else {
+    // blocks of kPeriodCheck iterations, the cycle test after each full block
+    for (uint32_t base = 0; base < max_iter; base += kPeriodCheck) {
+      const uint32_t len = max_iter - base < kPeriodCheck ? max_iter - base : kPeriodCheck;
+      for (uint32_t j = 0; j < len; ++j)
+        if (!iterate()) return;
+      if (len < kPeriodCheck) return;
+      // state after iteration base + kPeriodCheck
+  #pragma unroll
       for (int p = 0; p < P; ++p) {
         const long long zb = __double_as_longlong(zr[p]), wb = __double_as_longlong(zi[p]);
         if (live[p] && zb == sr[p] && wb == si[p]) {
@@ -175,8 +188,8 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
           live[p] = false;
         }
       }
-      if (i + 1 == save_at) {
-#pragma unroll
+      if (base + kPeriodCheck == save_at) {
+  #pragma unroll
         for (int p = 0; p < P; ++p) {
           sr[p] = __double_as_longlong(zr[p]);
           si[p] = __double_as_longlong(zi[p]);
