@@ -180,7 +180,7 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
         if (!iterate()) return;
       if (len < kPeriodCheck) return;
       // state after iteration base + kPeriodCheck
-  #pragma unroll
+#pragma unroll
       for (int p = 0; p < P; ++p) {
         const long long zb = __double_as_longlong(zr[p]), wb = __double_as_longlong(zi[p]);
         if (live[p] && zb == sr[p] && wb == si[p]) {
@@ -189,7 +189,7 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
         }
       }
       if (base + kPeriodCheck == save_at) {
-  #pragma unroll
+#pragma unroll
         for (int p = 0; p < P; ++p) {
           sr[p] = __double_as_longlong(zr[p]);
           si[p] = __double_as_longlong(zi[p]);
