@@ -259,9 +259,10 @@ def _dot_launch(st, v, items, ticket):
 
 
 def heat_block() -> int:
-    """Steps fused per HBM pass by the heat builtin (OFL_HEAT_TB, default 64 —
-    the fastest measured schedule, profiles/r01_heat_sweep.txt)."""
-    return max(1, min(128, int(os.environ.get("OFL_HEAT_TB", "64"))))
+    """Most steps fused per HBM pass by the heat builtin (OFL_HEAT_TB, default
+    72 — the fastest measured cap, profiles/r01_heat_sweep.txt; the C side
+    spreads the steps evenly over the fewest passes of the right parity)."""
+    return max(1, min(128, int(os.environ.get("OFL_HEAT_TB", "72"))))
 
 
 def _heat_oob(v, items):

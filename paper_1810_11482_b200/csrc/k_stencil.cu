@@ -526,16 +526,17 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
   const int sms = ofl::num_sms(s->dev);
   double* src = x;
   double* dst = y;
-  uint64_t left = steps;
   const size_t smem = sizeof(double) * 2 * (kTile + 2 * 64);
   // per-device attribute; cheap to (re)apply
   cudaFuncSetAttribute(k_heat_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // Pass schedule: full passes of tb steps plus a remainder; the number of
-  // passes must have the parity of `steps` so the state ends where the
-  // single-step ping-pong would leave it (x if steps is even, else y).
-  uint64_t full = steps / (uint64_t)tb, rem = steps % (uint64_t)tb;
-  uint64_t passes = full + (rem ? 1 : 0);
-  bool split = (passes & 1) != (steps & 1);  // split one pass into (k-1, 1)
+  // Pass schedule: the fewest passes of at most tb steps whose count has the
+  // parity of `steps` (each pass swaps the buffers, so the state must end
+  // where the single-step ping-pong would leave it: x if steps is even, else
+  // y), with the steps spread evenly over them — no short remainder pass and
+  // no extra single-step pass to fix the parity.
+  uint64_t passes = (steps + (uint64_t)tb - 1) / (uint64_t)tb;
+  if ((passes & 1) != (steps & 1)) ++passes;
+  const uint64_t base_k = passes ? steps / passes : 0, longer = passes ? steps % passes : 0;
   uint64_t launches = 0;
   auto run_pass = [&](int k) -> cudaError_t {
     if (k == 1) {
@@ -594,18 +595,10 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
     dst = t;
     return cudaPeekAtLastError();
   };
-  while (left > 0) {
-    int k = (uint64_t)tb < left ? tb : (int)left;
-    cudaError_t e;
-    if (split && k >= 2) {
-      e = run_pass(k - 1);
-      if (e == cudaSuccess) e = run_pass(1);
-      split = false;
-    } else {
-      e = run_pass(k);
-    }
+  for (uint64_t i = 0; i < passes; ++i) {
+    const int k = (int)(base_k + (i < longer ? 1 : 0));
+    cudaError_t e = run_pass(k);
     if (e != cudaSuccess) return ofl::cuda_error(e, "heat launch");
-    left -= (uint64_t)k;
   }
   ofl::count_launch(launches);
   return q.finish(ticket);
