@@ -141,7 +141,7 @@ def heat_cfg(rt, dev, out, steps=1000, n=1 << 28):
     Y = dev.create_buffer(n * 8).get()
     x = np.random.default_rng(20180214).random(n)
     finals = {}
-    for tb in (1, 8, 16, 32, 64):
+    for tb in (1, 8, 16, 32, 64, 72):  # 72 = the default cap
         os.environ["OFL_HEAT_TB"] = str(tb)
         Xs = dev.create_buffer(xs.nbytes).get()
         Ys = dev.create_buffer(xs.nbytes).get()
