@@ -83,6 +83,12 @@ void* ofl_stream_handle(ofl_stream* s);
  *      (device.py:217-228, buffer.py:26-38); device memory is zero-filled
  *      like np.zeros (buffer.py:32) ----------------------------------------- */
 int ofl_malloc(int dev, uint64_t bytes, void** dptr);
+/* CUDA IPC: share a device allocation (from ofl_malloc) with the other
+ * processes of the node (one process per GPU); handles are 64 bytes.  Used
+ * by the fused cross-process reduction (collectives.ProcessPeerGroup). */
+int ofl_ipc_handle(void* dptr, char* out64);
+int ofl_ipc_open(int dev, const char* handle64, void** dptr);
+int ofl_ipc_close(int dev, void* dptr);
 int ofl_free(int dev, void* dptr);
 int ofl_host_alloc(uint64_t bytes, void** hptr); /* pinned, portable */
 int ofl_host_free(void* hptr);

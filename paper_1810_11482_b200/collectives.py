@@ -154,3 +154,67 @@ class PeerGroup:
             toks.append(st.token(ticket.value))
         self.round += 1
         return when_all(toks)
+
+
+class ProcessPeerGroup:
+    """The fused cross-device reduction for one process per GPU (torchrun):
+    every rank allocates its exchange block, the 64-byte CUDA IPC handles
+    travel over torch.distributed (host side only, once), and each rank maps
+    the others' blocks — the reduction kernel then stores into and waits on
+    peer memory exactly as in ``PeerGroup``, with no collective call on the
+    data path."""
+
+    def __init__(self, rt, device, group=None):
+        import torch.distributed as dist
+
+        lib = _native.load()
+        self._rt = rt
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if not 1 <= self.world <= 16:
+            raise BadArgsError("a peer group has 1..16 members")
+        self.block = device.create_buffer(lib.ofl_xchg_bytes()).get()
+        obj = rt.local._buffer(self.block.gid)
+        self.ordinal = obj.device.ordinal
+        handle = ctypes.create_string_buffer(64)
+        _native.check(lib.ofl_ipc_handle(obj.ptr, handle), "ipc handle")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        ptrs = []
+        self._opened = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(obj.ptr)
+                continue
+            p = ctypes.c_void_p()
+            _native.check(lib.ofl_ipc_open(self.ordinal, h, ctypes.byref(p)), "ipc open")
+            self._opened.append(p.value)
+            ptrs.append(p.value)
+        self.ptrs = (ctypes.c_void_p * self.world)(*ptrs)
+        # the mapped peers are reached through IPC mappings: no extra peer
+        # enabling on this side (cudaIpcMemLazyEnablePeerAccess did it)
+        self.ordinals = (ctypes.c_int * self.world)(*([self.ordinal] * self.world))
+        self.round = 0
+        dist.barrier(group=group)  # every block exists and is mapped before use
+
+    def dot_f32(self, a_buf, b_buf, out_buf, n: int) -> CompletionToken:
+        """This rank's shard dot, summed across the ranks inside the kernel;
+        out_buf's first f64 holds the total (identical bits on every rank)."""
+        lib = _native.load()
+        local = self._rt.local
+        A, B, R = (local._buffer(x.gid) for x in (a_buf, b_buf, out_buf))
+        if n > min(A.elements("buffer_f32"), B.elements("buffer_f32")) or R.size_bytes < 8:
+            raise BadArgsError("shard larger than its buffers")
+        st = A.device.stream(0)
+        ticket = ctypes.c_uint64()
+        _native.check(lib.ofl_dot_f32_allreduce(
+            st.ptr, A.ptr, B.ptr, R.ptr, n, self.rank, self.world, self.ptrs, self.ordinals,
+            self.round, ctypes.byref(ticket)), "fused dot allreduce")
+        self.round += 1
+        return st.token(ticket.value)
+
+    def close(self) -> None:
+        lib = _native.load()
+        for p in self._opened:
+            lib.ofl_ipc_close(self.ordinal, p)
+        self._opened = []

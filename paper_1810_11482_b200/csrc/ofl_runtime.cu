@@ -276,6 +276,36 @@ uint64_t ofl_stream_done(ofl_stream* s) { return s->done.load(std::memory_order_
 void* ofl_stream_handle(ofl_stream* s) { return (void*)s->cs; }
 
 // --------------------------------------------------------------- memory ---
+// ------------------------------------------------------------- CUDA IPC ---
+// Device allocations shared between the processes of one node (one process
+// per GPU under torchrun): the owner exports a handle, the others map it and
+// reach the memory over NVLink (peer access enabled lazily by the driver).
+int ofl_ipc_handle(void* dptr, char* out64) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dptr);
+  if (e != cudaSuccess) return cuda_error(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  memcpy(out64, &h, sizeof(h));
+  return OFL_OK;
+}
+
+int ofl_ipc_open(int dev, const char* handle64, void** dptr) {
+  cudaError_t e = use_device(dev);
+  if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_error(e, "cudaIpcOpenMemHandle");
+  return OFL_OK;
+}
+
+int ofl_ipc_close(int dev, void* dptr) {
+  cudaError_t e = use_device(dev);
+  if (e == cudaSuccess) e = cudaIpcCloseMemHandle(dptr);
+  if (e != cudaSuccess) return cuda_error(e, "cudaIpcCloseMemHandle");
+  return OFL_OK;
+}
+
 int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   if (bytes == 0) return set_error(OFL_ERR_BAD_ARGS, "buffer size must be positive");
   cudaError_t e = use_device(dev);

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """BASELINE config 4: partitioned fp32 dot product, N = 2^31 total, across
-1/2/4/8 GPUs (strong scaling) with one NCCL allreduce per step.
+1/2/4/8 GPUs (strong scaling); the per-GPU partials are combined inside the
+reduction kernel over peer memory (default) or by one NCCL allreduce.
 
-    torchrun --nproc-per-node G --master-addr 127.0.0.1 scripts/bench_dot_dist.py [--n 2147483648]
+    torchrun --nproc-per-node G --master-addr 127.0.0.1 scripts/bench_dot_dist.py [--elements 2147483648] [--combine fused|nccl]
 
 Each rank owns a contiguous shard (bench/decomp.shard_bounds), reduces it
 with the dot_f32 builtin into an fp64 scalar on the device, and an
@@ -28,9 +29,12 @@ import numpy as np  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, default=1 << 31)
+    ap.add_argument("--elements", type=int, default=1 << 31)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--combine", choices=("fused", "nccl"), default="fused",
+                    help="fused: partials exchanged inside the reduction kernel over peer memory "
+                         "(CUDA IPC mappings); nccl: dot_f32 then one ncclAllReduce")
     args = ap.parse_args()
 
     import torch
@@ -39,7 +43,7 @@ def main():
     import oracle
     from paper_1810_11482_b200 import Runtime, _native
     from paper_1810_11482_b200.bench import decomp
-    from paper_1810_11482_b200.collectives import Communicator
+    from paper_1810_11482_b200.collectives import Communicator, ProcessPeerGroup
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -49,7 +53,7 @@ def main():
     lib = _native.load()
     with Runtime(devices=[local % max(1, _native.device_count())]) as rt:
         dev = rt.get_all_devices().get()[0]
-        lo, hi = decomp.shard_bounds(args.n, world)[rank : rank + 2]
+        lo, hi = decomp.shard_bounds(args.elements, world)[rank : rank + 2]
         m = hi - lo
         rng = np.random.default_rng(20180214 + rank)
         A = dev.create_buffer(max(4, m * 4)).get()
@@ -64,13 +68,20 @@ def main():
             A.enqueue_write(off * 4, a)
             B.enqueue_write(off * 4, b).get()
             part += oracle.dot_f32(a, b, threads=0)
-        comm = (Communicator.from_process_group(rt, dev) if world > 1
-                else Communicator.single_process(rt, [dev]))
+        comm = group = None
+        if args.combine == "fused" and world > 1:
+            group = ProcessPeerGroup(rt, dev)
+        else:
+            comm = (Communicator.from_process_group(rt, dev) if world > 1
+                    else Communicator.single_process(rt, [dev]))
         prog = dev.create_builtin_program().get()
         prog.build("dot_f32").get()
         grid = (max(1, m // 256), 1, 1)
 
         def step():
+            if group is not None:
+                group.dot_f32(A, B, R, m)
+                return
             prog.run([A, B, R, m], "dot_f32", grid, (256, 1, 1))
             if comm is not None:
                 comm.allreduce([R], count=1, dtype="f64")
@@ -103,14 +114,19 @@ def main():
         if rank == 0:
             step_ms = job_ms / args.steps
             print(json.dumps({
-                "config": "dot f32 N=%d across %d GPU(s), NCCL allreduce" % (args.n, world),
+                "config": "dot f32 N=%d across %d GPU(s), %s" % (
+                    args.elements, world, "partials exchanged in-kernel over peer memory"
+                    if group is not None else "NCCL allreduce"),
                 "ms_per_step": round(step_ms, 4),
-                "gbs_whole_job": round(8.0 * args.n / (step_ms * 1e-3) / 1e9, 1),
+                "gbs_whole_job": round(8.0 * args.elements / (step_ms * 1e-3) / 1e9, 1),
                 "result": got, "oracle": total, "rel_err": abs(got - total) / abs(total),
                 "within_1e-5": abs(got - total) <= 1e-5 * abs(total),
             }), flush=True)
         if comm is not None:
             comm.close()
+        if group is not None:
+            dist.barrier()
+            group.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -74,5 +74,8 @@ int ofl_jit_launch(void* s, void* k, void** p, uint64_t b, int t, uint64_t* tk) 
 int ofl_jit_destroy(void* k) { (void)k; return 0; }
 int ofl_fill_ones(void* s, void* d, uint64_t n, uint64_t* t) { memset(d, 0xff, n); return op(s, t); }
 int ofl_d2h_rows(void* s, void* d, uint64_t dp, const void* x, uint64_t rb, uint64_t r, uint64_t* t) { for (uint64_t i = 0; i < r; ++i) memcpy((char*)d + i * dp, (const char*)x + i * rb, rb); return op(s, t); }
+int ofl_ipc_handle(void* d, char* o) { (void)d; memset(o, 0, 64); return 2; }
+int ofl_ipc_open(int dev, const char* h, void** d) { (void)dev; (void)h; (void)d; return 2; }
+int ofl_ipc_close(int dev, void* d) { (void)dev; (void)d; return 0; }
 int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
 int ofl_host_memcpy(void* d, const void* s, uint64_t n) { memcpy(d, s, n); return 0; }

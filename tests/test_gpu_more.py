@@ -313,3 +313,62 @@ def test_stream_fifo_random_schedules(dev):
         dev.synchronize().get(timeout=30)
         model[8:24] = data
         assert buf.enqueue_read(0, size).get(timeout=30) == bytes(model), schedule
+
+
+IPC_DOT_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import torch.distributed as dist
+import oracle
+from paper_1810_11482_b200 import Runtime
+from paper_1810_11482_b200.collectives import ProcessPeerGroup
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+n = 3_000_001
+rng = np.random.default_rng(7)
+a = rng.random(n, dtype=np.float32); b = rng.random(n, dtype=np.float32)
+lo, hi = n * rank // world, n * (rank + 1) // world
+with Runtime(devices=[0]) as rt:
+    dev = rt.get_all_devices().get()[0]
+    A = dev.create_buffer((hi - lo) * 4).get(); B = dev.create_buffer((hi - lo) * 4).get()
+    R = dev.create_buffer(8).get()
+    A.enqueue_write(0, np.ascontiguousarray(a[lo:hi])); B.enqueue_write(0, np.ascontiguousarray(b[lo:hi]))
+    grp = ProcessPeerGroup(rt, dev)
+    exp = oracle.dot_f32(a, b, threads=0)
+    vals = []
+    for _ in range(4):
+        grp.dot_f32(A, B, R, hi - lo).get(timeout=60)
+        vals.append(np.frombuffer(R.enqueue_read(0, 8).get(), np.float64)[0])
+    assert all(v.tobytes() == vals[0].tobytes() for v in vals)
+    assert abs(vals[0] - exp) <= 1e-12 * abs(exp), (vals[0], exp)
+    got = [None] * world
+    dist.all_gather_object(got, vals[0].tobytes())
+    assert len(set(got)) == 1
+    dist.barrier()
+    grp.close()
+print(f"rank {rank} ipc ok", flush=True)
+"""
+
+
+def test_dot_fused_across_processes_ipc():
+    """One process per device (two processes sharing GPU 0 here): exchange
+    blocks mapped through CUDA IPC, partials exchanged inside the kernel;
+    both ranks end with the identical total, within 1e-12 of the oracle."""
+    import socket
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", IPC_DOT_SCRIPT, repo], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=300) for p in procs]
+    for r, (out, err) in enumerate(outs):
+        assert f"rank {r} ipc ok" in out, out[-500:] + err[-2000:]
