@@ -25,7 +25,15 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+
+// read-only, L1-bypassing 128-bit load (as the STREAM kernels)
+__device__ __forceinline__ double2 ld_nc(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
 
 __device__ __forceinline__ double point(double l, double c, double r) {
   return __dadd_rn(__dadd_rn(__dmul_rn(0.5, l), c), __dmul_rn(0.5, r));
@@ -34,39 +42,167 @@ __device__ __forceinline__ double point(double l, double c, double r) {
 // m  = number of items that execute (min(n, grid*block of the .k launch))
 // hi = highest readable x index = min(m, n-1)
 // One-shot tiles (as the STREAM kernels: the block scheduler balances many
-// small CTAs better than a persistent grid): thread j owns cells 2j, 2j+1.
-__global__ void __launch_bounds__(kThreads) k_stencil(const double* __restrict__ x,
-                                                      double* __restrict__ y, uint64_t n,
-                                                      uint64_t m) {
+// CTAs better than a persistent grid): a CTA of T threads covers U*T cell
+// pairs; thread t owns pairs base + t + u*T (cells 2j, 2j+1), so every load
+// instruction of a warp is one contiguous 512-byte run.  kPDL: programmatic
+// dependent launch (see k_stream.cu) for back-to-back steps.
+template <int T, int U, bool kPDL>
+__global__ void __launch_bounds__(T) k_stencil(const double* __restrict__ x,
+                                               double* __restrict__ y, uint64_t n, uint64_t m) {
+  if constexpr (kPDL) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const int lane = threadIdx.x & 31;
   const uint64_t hi = (m < n - 1) ? m : n - 1;
-  {
-    const uint64_t j = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  double edge[U];
+  double2 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t j = (uint64_t)blockIdx.x * (T * U) + (uint64_t)u * T + threadIdx.x;
     const uint64_t lo = 2 * j;
-    // the warp-edge neighbours are loaded together with the main vector, so
+    // the warp-edge neighbours are loaded together with the main vectors, so
     // a warp waits for one memory latency, not two
-    double edge = 0.0;
-    if (lane == 0 && lo >= 1 && lo - 1 <= hi) edge = x[lo - 1];
-    if (lane == 31 && lo + 2 <= hi) edge = x[lo + 2];
-    double2 v = make_double2(0.0, 0.0);
+    edge[u] = 0.0;
+    if (lane == 0 && lo >= 1 && lo - 1 <= hi) edge[u] = x[lo - 1];
+    if (lane == 31 && lo + 2 <= hi) edge[u] = x[lo + 2];
+    v[u] = make_double2(0.0, 0.0);
     if (lo + 1 <= hi) {
-      v = __ldcs(reinterpret_cast<const double2*>(x) + j);
+      v[u] = ld_nc(reinterpret_cast<const double2*>(x) + j);
     } else if (lo <= hi) {
-      v.x = x[lo];
+      v[u].x = x[lo];
     }
-    double left = __shfl_up_sync(0xffffffffu, v.y, 1);
-    double right = __shfl_down_sync(0xffffffffu, v.x, 1);
-    if (lane == 0) left = edge;
-    if (lane == 31) right = edge;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t j = (uint64_t)blockIdx.x * (T * U) + (uint64_t)u * T + threadIdx.x;
+    const uint64_t lo = 2 * j;
+    double left = __shfl_up_sync(0xffffffffu, v[u].y, 1);
+    double right = __shfl_down_sync(0xffffffffu, v[u].x, 1);
+    if (lane == 0) left = edge[u];
+    if (lane == 31) right = edge[u];
     if (lo < m) {
-      const double r0 = (lo == 0 || lo == n - 1) ? v.x : point(left, v.x, v.y);
+      const double r0 = (lo == 0 || lo == n - 1) ? v[u].x : point(left, v[u].x, v[u].y);
       if (lo + 1 < m) {
-        const double r1 = (lo + 1 == n - 1) ? v.y : point(v.x, v.y, right);
+        const double r1 = (lo + 1 == n - 1) ? v[u].y : point(v[u].x, v[u].y, right);
         __stcs(reinterpret_cast<double2*>(y) + j, make_double2(r0, r1));
       } else {
         y[lo] = r0;
       }
     }
+  }
+}
+
+// Shared-memory form: the CTA's U*T pairs are staged once in shared memory
+// with the two cells just outside the CTA's range (loaded by threads 0 and
+// T-1), so each cell's outer neighbours come from shared memory instead of a
+// warp-edge load per warp: 2 extra loads per 2*U*T cells instead of 2 per
+// 64 — the per-warp edge loads cost the shuffle form ~13% against a copy.
+template <int T, int U, bool kPDL>
+__global__ void __launch_bounds__(T) k_stencil_smem(const double* __restrict__ x,
+                                                    double* __restrict__ y, uint64_t n,
+                                                    uint64_t m) {
+  if constexpr (kPDL) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  constexpr int kCells = 2 * T * U;
+  __shared__ double tile[kCells + 2];  // tile[1 + i] = x[c0 + i]
+  const uint64_t hi = (m < n - 1) ? m : n - 1;  // highest readable index
+  const uint64_t c0 = (uint64_t)blockIdx.x * kCells;
+  double2 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t j = c0 / 2 + (uint64_t)u * T + threadIdx.x;
+    const uint64_t lo = 2 * j;
+    v[u] = make_double2(0.0, 0.0);
+    if (lo + 1 <= hi) v[u] = ld_nc(reinterpret_cast<const double2*>(x) + j);
+    else if (lo <= hi) v[u].x = x[lo];
+  }
+  if (threadIdx.x == 0) tile[0] = (c0 >= 1 && c0 - 1 <= hi) ? x[c0 - 1] : 0.0;
+  if (threadIdx.x == T - 1) tile[kCells + 1] = (c0 + kCells <= hi) ? x[c0 + kCells] : 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = 2 * (u * T + threadIdx.x);
+    tile[1 + i] = v[u].x;
+    tile[2 + i] = v[u].y;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = 2 * (u * T + threadIdx.x);
+    const uint64_t lo = c0 + i;
+    if (lo < m) {
+      const double left = tile[i], right = tile[i + 3];
+      const double r0 = (lo == 0 || lo == n - 1) ? v[u].x : point(left, v[u].x, v[u].y);
+      if (lo + 1 < m) {
+        const double r1 = (lo + 1 == n - 1) ? v[u].y : point(v[u].x, v[u].y, right);
+        __stcs(reinterpret_cast<double2*>(y + lo), make_double2(r0, r1));
+      } else {
+        y[lo] = r0;
+      }
+    }
+  }
+}
+
+template <int T, int U>
+void launch_stencil_smem(cudaStream_t cs, const double* x, double* y, uint64_t n, uint64_t m) {
+  const uint64_t cells = 2ull * T * U;
+  const unsigned blocks = (unsigned)((m + cells - 1) / cells);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(T);
+  cfg.stream = cs;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_stencil_smem<T, U, true>, x, y, n, m);
+}
+
+// single-step launch shape (OFL_STENCIL_VARIANT, sweeps; 2^28 cells, back
+// to back): 0 = shared-memory staging, 256 threads x 4 pairs, PDL (default:
+// 621 us/step, 6.91 TB/s — copy speed); shuffle form 1 = 256 x 1 (the first
+// version, 713 us), 2 = 512 x 1 + PDL (742), 3 = 256 x 4 + PDL (770),
+// 7 = 512 x 2 + PDL (706); smem form 4 = 512 x 2 (630), 5 = 512 x 1 (786)
+int stencil_variant() {
+  static int v = [] {
+    const char* e = getenv("OFL_STENCIL_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int T, int U, bool kPDL>
+void launch_stencil_t(cudaStream_t cs, const double* x, double* y, uint64_t n, uint64_t m) {
+  const uint64_t npairs = (m + 1) >> 1;
+  const unsigned blocks = (unsigned)((npairs + (uint64_t)T * U - 1) / ((uint64_t)T * U));
+  if (!kPDL) {
+    k_stencil<T, U, false><<<blocks, T, 0, cs>>>(x, y, n, m);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(T);
+  cfg.stream = cs;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_stencil<T, U, true>, x, y, n, m);
+}
+
+void launch_stencil(cudaStream_t cs, const double* x, double* y, uint64_t n, uint64_t m) {
+  switch (stencil_variant()) {
+    case 1: launch_stencil_t<256, 1, false>(cs, x, y, n, m); break;
+    case 2: launch_stencil_t<512, 1, true>(cs, x, y, n, m); break;
+    case 3: launch_stencil_t<256, 4, true>(cs, x, y, n, m); break;
+    case 4: launch_stencil_smem<512, 2>(cs, x, y, n, m); break;
+    case 5: launch_stencil_smem<512, 1>(cs, x, y, n, m); break;
+    case 7: launch_stencil_t<512, 2, true>(cs, x, y, n, m); break;
+    default: launch_stencil_smem<256, 4>(cs, x, y, n, m); break;
   }
 }
 
@@ -470,9 +606,7 @@ extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
   if (m) {
-    const uint64_t npairs = (m + 1) >> 1;
-    uint64_t blocks = (npairs + kThreads - 1) / kThreads;
-    k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(x, y, n, m);
+    launch_stencil(s->cs, x, y, n, m);
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return ofl::cuda_error(e, "stencil launch");
     ofl::count_launch();
@@ -540,9 +674,7 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
   uint64_t launches = 0;
   auto run_pass = [&](int k) -> cudaError_t {
     if (k == 1) {
-      uint64_t npairs = (n + 1) >> 1;
-      uint64_t blocks = (npairs + kThreads - 1) / kThreads;
-      k_stencil<<<(unsigned)blocks, kThreads, 0, s->cs>>>(src, dst, n, n);
+      launch_stencil(s->cs, src, dst, n, n);
     } else if (heat_kernel() == 1) {
       const uint64_t ntiles = (n + kTile - 1) / kTile;
       uint64_t blocks = ntiles < (uint64_t)sms * 2 ? ntiles : (uint64_t)sms * 2;
