@@ -171,6 +171,72 @@ __global__ void __launch_bounds__(kThreads) k_stencil2d_batch(const double* __re
   }
 }
 
+// CTA form of the batch kernel: the CTA's 8 warps sit side by side (512
+// columns x RB rows), so a warp's west / east strip-edge cells are its
+// neighbour warps' first / last columns, exchanged through shared memory;
+// only the CTA's two outer strips load edge cells from global memory (2 per
+// 8 warps instead of 2 per warp — per-warp edge loads cost the 1-D stencil
+// 13% against a copy, profiles/r01_stencil2d_sweep.txt).
+template <int RB>
+__global__ void __launch_bounds__(kThreads) k_stencil2d_cta(const double* __restrict__ x,
+                                                            double* __restrict__ y, uint32_t w,
+                                                            uint32_t h, uint64_t m, uint64_t lx,
+                                                            uint32_t cta_cols) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int kWarps = kThreads / 32;
+  __shared__ double s_first[kWarps][RB], s_last[kWarps][RB];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const uint32_t bx = blockIdx.x % cta_cols, by = blockIdx.x / cta_cols;
+  const uint32_t c0 = bx * (64u * kWarps) + 64u * (uint32_t)wq;
+  const int64_t r0 = (int64_t)by * RB;
+  const uint32_t j = c0 + 2u * (uint32_t)lane;
+  const bool mine = j < w;
+  double2 v[RB + 2];  // rows r0-1 .. r0+RB
+#pragma unroll
+  for (int k = 0; k < RB + 2; ++k) {
+    const int64_t r = r0 - 1 + k;
+    v[k] = (mine && r >= 0 && r < h) ? ld2(x, (uint64_t)r * w + j, lx) : make_double2(0.0, 0.0);
+  }
+  // outer strips only: lane k holds the edge cell of row r0+k
+  const int64_t re = r0 + lane;
+  const bool erow = lane < RB && re < h;
+  const double eLv = (wq == 0 && erow && c0 > 0) ? ld1(x, (uint64_t)re * w + c0 - 1, lx) : 0.0;
+  const double eRv = (wq == kWarps - 1 && erow && c0 + 64 < w)
+                         ? ld1(x, (uint64_t)re * w + c0 + 64, lx) : 0.0;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < RB; ++k) s_first[wq][k] = v[k + 1].x;
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < RB; ++k) s_last[wq][k] = v[k + 1].y;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < RB; ++k) {
+    const int64_t i = r0 + k;
+    const double2 up = v[k], cur = v[k + 1], down = v[k + 2];
+    double west = __shfl_up_sync(0xffffffffu, cur.y, 1);
+    double east = __shfl_down_sync(0xffffffffu, cur.x, 1);
+    const double wl = __shfl_sync(0xffffffffu, eLv, k);
+    const double er = __shfl_sync(0xffffffffu, eRv, k);
+    if (lane == 0) west = wq > 0 ? s_last[wq - 1][k] : wl;
+    if (lane == 31) east = wq < kWarps - 1 ? s_first[wq + 1][k] : er;
+    const uint64_t g = (uint64_t)i * w + j;
+    if (i < h && mine && g < m) {
+      const bool edge_row = (i == 0) || (i == (int64_t)h - 1);
+      const double o0 = (edge_row || j == 0) ? cur.x : interior(up.x, west, cur.y, down.x);
+      const double o1 = (edge_row || j + 1 == w - 1) ? cur.y : interior(up.y, cur.x, east, down.y);
+      if (g + 1 < m) {
+        __stcs(reinterpret_cast<double2*>(y + g), make_double2(o0, o1));
+      } else {
+        y[g] = o0;
+      }
+    }
+  }
+}
+
 // TMA-staged form (full grids, w even, w*h < 2^32): persistent CTAs walk
 // 64-column x 32-row output tiles; one elected thread stages each tile's 34
 // input rows (cols c0-2 .. c0+65, clipped to the grid; 16-byte aligned) into
@@ -336,9 +402,10 @@ void launch_pdl(void (*kernel)(KArgs...), unsigned blocks, cudaStream_t cs, Args
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// OFL_STENCIL2D_VARIANT (sweeps): 0 = batch of 8 rows per warp (default,
-// profiles/r01_stencil2d_sweep.txt), 1 = row marching (32 rows), 2/3/4 =
-// batch of 16/4/12 rows, 5 = TMA-staged tiles (4 stages; full grids)
+// OFL_STENCIL2D_VARIANT (sweeps, profiles/r01_stencil2d_sweep.txt): 0 = CTA
+// form, 8 warps side by side x 8 rows (default), 6 = per-warp batch of 8
+// rows, 1 = row marching (32 rows), 2/3/4 = batch of 16/4/12 rows, 5 =
+// TMA-staged tiles (4 stages; full grids)
 int stencil2d_variant() {
   static int v = [] {
     const char* e = getenv("OFL_STENCIL2D_VARIANT");
@@ -371,6 +438,12 @@ extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t
       cudaStream_t cs = s->cs;
       if (v == 5 && m == cells) {
         launch_stencil2d_tma<4>(cs, ofl::num_sms(s->dev), x, y, w, h);
+      } else if (v == 0) {
+        constexpr int RB = 8;
+        const uint32_t cta_cols = (w + 64u * (kThreads / 32) - 1) / (64u * (kThreads / 32));
+        const uint64_t row_blocks = (rows_needed + RB - 1) / RB;
+        launch_pdl(k_stencil2d_cta<RB>, (unsigned)(cta_cols * row_blocks), cs, x, y, w, h, m,
+                   x_elems, cta_cols);
       } else if (v == 1)
         k_stencil2d_march<<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
       else if (v == 2)
@@ -379,7 +452,7 @@ extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t
         k_stencil2d_batch<4><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
       else if (v == 4)
         k_stencil2d_batch<12><<<blocks, kThreads, 0, cs>>>(x, y, w, h, m, x_elems, col_chunks);
-      else
+      else  // v == 6
         launch_pdl(k_stencil2d_batch<8, false, true>, blocks, cs, x, y, w, h, m, x_elems,
                    col_chunks, SlabRows{});
     } else {
