@@ -182,7 +182,7 @@ int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, in
 /* One slab pass of the multi-GPU heat equation (BASELINE config 2; the
  * reference has no multi-device stencil — harness.py:199-230 is single-device,
  * its cross-device path is copy() through the host, handles.py:119-145):
- * k (1..64) stencil.k steps of slab x -> y (length n, local cells 0 and n-1
+ * k (1..128) stencil.k steps of slab x -> y (length n, local cells 0 and n-1
  * held fixed), writing y only for the owned cells [own_lo, own_hi), and the
  * first / last h owned cells also straight into left_ghost[0..h) /
  * right_ghost[0..h) — the neighbouring slabs' ghost cells, on devices

@@ -460,7 +460,7 @@ class HeatSlabs:
     endpoints stay fixed because a slab's outer end is either the true
     endpoint or a ghost that is overwritten before use.
 
-    Exchange (``fused``, default when halo <= 64 and all devices are in this
+    Exchange (``fused``, default when halo <= 128 and all devices are in this
     process): the pass kernel itself stores its first / last `halo` owned
     cells into the neighbours' ghost cells through peer pointers (NVLink
     stores, ``ofl_heat_slab``), and each device's next pass waits on its two
@@ -494,9 +494,9 @@ class HeatSlabs:
             A.enqueue_write(0, local.tobytes())
             self.a.append(A)
             self.b.append(B)
-        self.fused = (halo <= 64) if fused is None else bool(fused)
-        if self.fused and halo > 64:
-            raise BadArgsError("the fused exchange needs halo <= 64 (one pass per exchange)")
+        self.fused = (halo <= 128) if fused is None else bool(fused)
+        if self.fused and halo > 128:
+            raise BadArgsError("the fused exchange needs halo <= 128 (one pass per exchange)")
         self.progs = None if self.fused else [_builtin(d, "heat") for d in self.devices]
 
     def _exchange(self, cur: list) -> list:

@@ -740,8 +740,8 @@ extern "C" int ofl_heat_slab(ofl_stream* s, const double* x, double* y, uint64_t
                              uint64_t own_lo, uint64_t own_hi, double* left_ghost, int left_dev,
                              double* right_ghost, int right_dev, uint64_t h, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
-  if (n < 1 || k < 1 || k > 64)
-    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab needs n >= 1 and 1 <= k <= 64");
+  if (n < 1 || k < 1 || k > 128)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab needs n >= 1 and 1 <= k <= 128");
   if (own_lo > own_hi || own_hi > n || h > own_hi - own_lo)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: bad owned range / halo");
   if (x == y) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: x and y must differ");

@@ -77,7 +77,7 @@ def test_heat_multi_device_temporal_halo(rt2, halo, steps, fused):
     assert got.tobytes() == oracle.heat(x, steps, threads=0).tobytes()
 
 
-@pytest.mark.parametrize("parts,halo,steps", [(4, 64, 301), (5, 3, 40), (3, 64, 64)])
+@pytest.mark.parametrize("parts,halo,steps", [(4, 64, 301), (5, 3, 40), (3, 64, 64), (2, 96, 250)])
 def test_heat_fused_exchange_many_slabs(parts, halo, steps):
     """Peer-store halo exchange between several slabs (logical devices on
     GPU 0, each with its own streams, so passes really run concurrently and
