@@ -238,22 +238,25 @@ class Runtime:
         raise UnknownGidError(f"{gid} names an unknown locality")
 
     def local_program(self, gid: GlobalId):
-        """(registry objects, ProgramObject) for a program owned by this
-        process, else None — the handles' fast launch path (handles.py)."""
+        """(registry, generation, ProgramObject) for a program owned by this
+        process, else None — the handles' fast launch path (handles.py); the
+        resolution stays valid while ``registry.generation`` is unchanged."""
         if gid.locality_id != self.registry.self_locality_id:
             return None
         try:
-            return self.registry._objects, self.local._program(gid)
+            reg = self.registry
+            return reg, reg.generation, self.local._program(gid)
         except Exception:  # noqa: BLE001 - the general path reports it
             return None
 
     def local_buffer(self, gid: GlobalId):
-        """(registry objects, BufferObject) for a buffer owned by this process,
-        else None — the handles' fast write path (handles.py)."""
+        """(registry, generation, BufferObject) for a buffer owned by this
+        process, else None — the handles' fast paths (handles.py)."""
         if gid.locality_id != self.registry.self_locality_id:
             return None
         try:
-            return self.registry._objects, self.local._buffer(gid)
+            reg = self.registry
+            return reg, reg.generation, self.local._buffer(gid)
         except Exception:  # noqa: BLE001 - the general path reports it
             return None
 
