@@ -372,3 +372,20 @@ def test_dot_fused_across_processes_ipc():
     outs = [p.communicate(timeout=300) for p in procs]
     for r, (out, err) in enumerate(outs):
         assert f"rank {r} ipc ok" in out, out[-500:] + err[-2000:]
+
+
+def test_c_abi_example_runs(tmp_path):
+    """examples/triad_c_abi.c: a pure-C host drives libofl.so (streams,
+    pinned memory, copies, the triad, ticket wait) — the boundary a cgo /
+    JNI / N-API binding of the reference's dispatch seam would use."""
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(repo, "paper_1810_11482_b200", "lib")
+    exe = str(tmp_path / "triad_c")
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-I", os.path.join(repo, "include"),
+                    os.path.join(repo, "examples", "triad_c_abi.c"), "-L", lib, "-lofl",
+                    f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout
