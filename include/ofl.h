@@ -89,6 +89,15 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr);
 int ofl_ipc_handle(void* dptr, char* out64);
 int ofl_ipc_open(int dev, const char* handle64, void** dptr);
 int ofl_ipc_close(int dev, void* dptr);
+/* Device-side ordering between processes (ofl_gate.cu): a one-thread kernel
+ * that publishes a 64-bit completion counter (after a system fence), and one
+ * that polls other ranks' counters (device pointers, e.g. IPC-mapped; the
+ * pointer array itself lives in device memory) until each reaches `target`,
+ * recording a timeout in *status after ~20 s.  Used by the multi-process
+ * heat slabs (bench.ProcessHeatSlabs) so no host round trip orders a pass. */
+int ofl_gate_signal(ofl_stream* s, unsigned long long* counter, uint64_t value, uint64_t* ticket);
+int ofl_gate_wait(ofl_stream* s, const unsigned long long* const* counters_dev, int count,
+                  uint64_t target, unsigned long long* status, uint64_t* ticket);
 int ofl_free(int dev, void* dptr);
 int ofl_host_alloc(uint64_t bytes, void** hptr); /* pinned, portable */
 int ofl_host_free(void* hptr);

@@ -65,6 +65,8 @@ _SIGNATURES = {
     "ofl_ipc_handle": (c_int, [c_void_p, c_char_p]),
     "ofl_ipc_open": (c_int, [c_int, c_char_p, POINTER(c_void_p)]),
     "ofl_ipc_close": (c_int, [c_int, c_void_p]),
+    "ofl_gate_signal": (c_int, [_c_stream, c_void_p, c_uint64, _u64p]),
+    "ofl_gate_wait": (c_int, [_c_stream, c_void_p, c_int, c_uint64, c_void_p, _u64p]),
     "ofl_d2h_rows": (c_int, [_c_stream, c_void_p, c_uint64, c_void_p, c_uint64, c_uint64, _u64p]),
     "ofl_d2d": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_h2d_pageable": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),

@@ -545,6 +545,128 @@ class HeatSlabs:
         return out
 
 
+class ProcessHeatSlabs:
+    """Config 2 with one process per GPU (torchrun): rank g owns slab g of
+    the 1-D heat equation.  The slabs' buffers and a per-rank completion
+    counter are shared through CUDA IPC once at construction; each pass is
+    (1) a one-thread gate kernel that waits on the device until both
+    neighbours' counters show the previous pass done, (2) the slab pass with
+    its boundary strips stored straight into the neighbours' ghost cells
+    (ofl_heat_slab over the IPC mappings), (3) a one-thread kernel that
+    publishes this rank's counter — no host synchronisation per exchange."""
+
+    def __init__(self, rt, device: DeviceHandle, x: np.ndarray, halo: int = 64, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from .. import _native
+
+        if not 1 <= halo <= 128:
+            raise BadArgsError("halo must be 1..128")
+        lib = _native.load()
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.group, self.halo, self.n = group, halo, x.size
+        try:
+            self.layout = decomp.slabs(x.size, self.world, halo)
+        except ValueError as exc:
+            raise BadArgsError(str(exc)) from None
+        self.bounds = decomp.shard_bounds(x.size, self.world)
+        sl = self.layout[self.rank]
+        local = np.ascontiguousarray(np.asarray(x, dtype=np.float64)[sl.start : sl.start + sl.length])
+        self.bufs = [device.create_buffer(local.nbytes).get() for _ in range(2)]
+        self.bufs[0].enqueue_write(0, local.tobytes())
+        self.block = device.create_buffer(64).get()  # [0] counter, [8] status
+        objs = [rt.local._buffer(b.gid) for b in (*self.bufs, self.block)]
+        self.ordinal = objs[0].device.ordinal
+        self.stream = objs[0].device.stream(0)
+        self._ptrs = [o.ptr for o in objs]
+        mine = []
+        for o in objs:
+            h = ctypes.create_string_buffer(64)
+            _native.check(lib.ofl_ipc_handle(o.ptr, h), "ipc handle")
+            mine.append(h.raw)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.peer = {}  # rank -> (bufA, bufB, block) device pointers in this process
+        for r in (self.rank - 1, self.rank + 1):
+            if 0 <= r < self.world:
+                ptrs = []
+                for h in allh[r]:
+                    p = ctypes.c_void_p()
+                    _native.check(lib.ofl_ipc_open(self.ordinal, h, ctypes.byref(p)), "ipc open")
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                self.peer[r] = ptrs
+        counters = [self.peer[r][2] for r in sorted(self.peer)]
+        self.gate = device.create_buffer(8 * max(1, len(counters))).get()
+        if counters:
+            self.gate.enqueue_write(0, np.array(counters, dtype=np.uint64).tobytes()).get()
+        self._gate_ptr = rt.local._buffer(self.gate.gid).ptr
+        self._ncounters = len(counters)
+        self.passes = 0
+        self.cur = 0  # index of the buffer holding the current state
+        dist.barrier(group=group)  # every mapping exists before anyone stores
+
+    def run(self, steps: int):
+        import ctypes
+
+        from .. import _native
+
+        lib = self.stream.lib
+        st, h = self.stream, self.halo
+        sl, g = self.layout[self.rank], self.rank
+        ticket = ctypes.c_uint64()
+        done = 0
+        while done < steps:
+            k = min(h, steps - done)
+            nxt = 1 - self.cur
+            _native.check(lib.ofl_gate_wait(st.ptr, self._gate_ptr, self._ncounters, self.passes,
+                                            self._ptrs[2] + 8, ctypes.byref(ticket)), "gate wait")
+            up = down = None
+            if g - 1 in self.peer:
+                left = self.layout[g - 1]
+                up = self.peer[g - 1][nxt] + (left.left + left.owned) * 8
+            if g + 1 in self.peer:
+                down = self.peer[g + 1][nxt]
+            _native.check(lib.ofl_heat_slab(
+                st.ptr, self._ptrs[self.cur], self._ptrs[nxt], sl.length, k, sl.left,
+                sl.left + sl.owned, up, self.ordinal, down, self.ordinal, h,
+                ctypes.byref(ticket)), "heat slab pass")
+            self.passes += 1
+            _native.check(lib.ofl_gate_signal(st.ptr, self._ptrs[2], self.passes,
+                                              ctypes.byref(ticket)), "gate signal")
+            self.cur = nxt
+            done += k
+        return st.token(ticket.value) if steps else None
+
+    def gather(self) -> np.ndarray:
+        """The whole vector on every rank (host all-gather of the owned cells)."""
+        import torch.distributed as dist
+
+        sl = self.layout[self.rank]
+        mine = np.frombuffer(self.bufs[self.cur].enqueue_read(sl.left * 8, sl.owned * 8).get(),
+                             np.float64)
+        status = np.frombuffer(self.block.enqueue_read(8, 8).get(), np.uint64)[0]
+        if status:
+            raise RuntimeError("heat slab gate timed out waiting for a neighbour")
+        parts = [None] * self.world
+        dist.all_gather_object(parts, mine, group=self.group)
+        return np.concatenate(parts)
+
+    def close(self) -> None:
+        import torch.distributed as dist
+
+        from .. import _native
+
+        dist.barrier(group=self.group)  # nobody stores into mappings being closed
+        lib = _native.load()
+        for p in self._opened:
+            lib.ofl_ipc_close(self.ordinal, p)
+        self._opened = []
+
+
 class Heat2DSlabs:
     """Row-slab decomposition of the 2-D heat equation (kernels/stencil2d.k)
     over several devices in this process.  Slab g holds its owned rows plus

@@ -77,5 +77,7 @@ int ofl_d2h_rows(void* s, void* d, uint64_t dp, const void* x, uint64_t rb, uint
 int ofl_ipc_handle(void* d, char* o) { (void)d; memset(o, 0, 64); return 2; }
 int ofl_ipc_open(int dev, const char* h, void** d) { (void)dev; (void)h; (void)d; return 2; }
 int ofl_ipc_close(int dev, void* d) { (void)dev; (void)d; return 0; }
+int ofl_gate_signal(void* s, void* c, uint64_t v, uint64_t* t) { (void)c; (void)v; return op(s, t); }
+int ofl_gate_wait(void* s, const void* c, int n, uint64_t tg, void* st, uint64_t* t) { (void)c; (void)n; (void)tg; (void)st; return op(s, t); }
 int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
 int ofl_host_memcpy(void* d, const void* s, uint64_t n) { memcpy(d, s, n); return 0; }

@@ -389,3 +389,49 @@ def test_c_abi_example_runs(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 mismatches" in r.stdout
+
+
+IPC_HEAT_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import torch.distributed as dist
+import oracle
+from paper_1810_11482_b200 import Runtime
+from paper_1810_11482_b200.bench.harness import ProcessHeatSlabs
+dist.init_process_group("gloo")
+rank = dist.get_rank()
+x = np.random.default_rng(3).random(40_001)
+with Runtime(devices=[0]) as rt:
+    dev = rt.get_all_devices().get()[0]
+    slabs = ProcessHeatSlabs(rt, dev, x, halo=16)
+    slabs.run(45).get(timeout=120)
+    got = slabs.gather()
+    slabs.close()
+assert got.tobytes() == oracle.heat(x, 45, threads=0).tobytes()
+print(f"rank {rank} heat ipc ok", flush=True)
+"""
+
+
+def test_heat_slabs_across_processes_ipc():
+    """One process per device (two processes sharing GPU 0 here): slab
+    buffers and completion counters shared through CUDA IPC, passes ordered
+    by device-side gate kernels, halos stored straight into the neighbour's
+    ghost cells: bit-identical to the single-device heat equation."""
+    import socket
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", IPC_HEAT_SCRIPT, repo], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=300) for p in procs]
+    for r, (out, err) in enumerate(outs):
+        assert f"rank {r} heat ipc ok" in out, out[-500:] + err[-2000:]
