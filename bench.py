@@ -284,6 +284,20 @@ def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int, payload_bytes
         )
         return secs.value
 
+    def capi(steps: int) -> float:
+        # the product C-ABI (libofl tickets, same kernel launch) called from
+        # Python without futures: splits the overhead into C-ABI + futures
+        t = ctypes.c_uint64()
+        ref = ctypes.byref(t)
+        h2d, op, sp, src = lib.ofl_h2d, lib.ofl_stream_op, stream.ptr, payload.ctypes.data
+        dev.synchronize().get()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            h2d(sp, dptr, src, payload_bytes, ref)
+            op(sp, 3, aptr, bptr, cptr, 3.0, n, ref)
+        dev.synchronize().get()
+        return time.perf_counter() - t0
+
     def pipelined(steps: int) -> float:
         dev.synchronize().get()
         t0 = time.perf_counter()
@@ -305,15 +319,18 @@ def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int, payload_bytes
 
     # warm both paths
     raw(200, 0)
+    capi(200)
     pipelined(200)
     raw(100, 2)
     synced(100)
     out = {}
     t_raw = min(raw(steps_pipelined, 0) for _ in range(3))
+    t_capi = min(capi(steps_pipelined) for _ in range(3))
     t_fut = min(pipelined(steps_pipelined) for _ in range(3))
     out["pipelined_when_all"] = {
         "steps": steps_pipelined,
         "raw_us_per_step": t_raw / steps_pipelined * 1e6,
+        "c_abi_us_per_step": t_capi / steps_pipelined * 1e6,
         "futurized_us_per_step": t_fut / steps_pipelined * 1e6,
         "overhead_us_per_step": (t_fut - t_raw) / steps_pipelined * 1e6,
         "overhead_us_per_future": (t_fut - t_raw) / steps_pipelined / 2 * 1e6,

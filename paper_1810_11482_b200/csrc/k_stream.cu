@@ -318,6 +318,18 @@ cudaError_t launch(cudaStream_t st, int sms, double* a, const double* b, const d
 
 }  // namespace
 
+namespace ofl {
+cudaError_t stream_launch(cudaStream_t st, int sms, int op, double* a, const double* b,
+                          const double* c, double scalar, uint64_t n) {
+  switch (op) {
+    case OFL_STREAM_COPY: return launch<OFL_STREAM_COPY>(st, sms, a, b, c, scalar, n);
+    case OFL_STREAM_SCALE: return launch<OFL_STREAM_SCALE>(st, sms, a, b, c, scalar, n);
+    case OFL_STREAM_ADD: return launch<OFL_STREAM_ADD>(st, sms, a, b, c, scalar, n);
+    default: return launch<OFL_STREAM_TRIAD>(st, sms, a, b, c, scalar, n);
+  }
+}
+}  // namespace ofl
+
 extern "C" int ofl_stream_op(ofl_stream* s, int op, double* a, const double* b, const double* c,
                              double scalar, uint64_t n, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
@@ -327,14 +339,7 @@ extern "C" int ofl_stream_op(ofl_stream* s, int op, double* a, const double* b, 
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
   if (n) {
-    const int sms = ofl::num_sms(s->dev);
-    cudaError_t e;
-    switch (op) {
-      case OFL_STREAM_COPY: e = launch<OFL_STREAM_COPY>(s->cs, sms, a, b, c, scalar, n); break;
-      case OFL_STREAM_SCALE: e = launch<OFL_STREAM_SCALE>(s->cs, sms, a, b, c, scalar, n); break;
-      case OFL_STREAM_ADD: e = launch<OFL_STREAM_ADD>(s->cs, sms, a, b, c, scalar, n); break;
-      default: e = launch<OFL_STREAM_TRIAD>(s->cs, sms, a, b, c, scalar, n); break;
-    }
+    const cudaError_t e = ofl::stream_launch(s->cs, ofl::num_sms(s->dev), op, a, b, c, scalar, n);
     if (e != cudaSuccess) return ofl::cuda_error(e, "STREAM launch");
     ofl::count_launch();
   }

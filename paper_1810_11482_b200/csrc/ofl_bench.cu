@@ -7,16 +7,6 @@
 
 #include "ofl_internal.h"
 
-namespace {
-
-__global__ void k_triad_small(double* __restrict__ a, const double* __restrict__ b,
-                              const double* __restrict__ c, double s, uint64_t n) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = __dadd_rn(b[i], __dmul_rn(s, c[i]));
-}
-
-}  // namespace
-
 // FP64 issue-rate probe for the Mandelbrot roofline: independent DMUL and
 // DADD chains (no FMA — the bit-exact kernel may not contract either).
 __global__ void k_fp64_peak(double* out, double a, double b, int iters) {
@@ -79,13 +69,15 @@ extern "C" int ofl_bench_raw_chain(ofl_stream* s, void* dst, const void* src, ui
   if (e != cudaSuccess) return ofl::cuda_error(e, "cudaSetDevice");
   cudaEvent_t ev = nullptr;
   if (mode == 1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const int sms = ofl::num_sms(s->dev);
   cudaStreamSynchronize(s->cs);
   auto t0 = std::chrono::steady_clock::now();
   for (uint64_t k = 0; k < steps; ++k) {
     if (mode == 1 && k) cudaStreamWaitEvent(s->cs, ev, 0);
     cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s->cs);
-    k_triad_small<<<blocks ? blocks : 1, 256, 0, s->cs>>>(a, b, c, 3.0, n);
+    // the same kernel and launch (attributes included) ofl_stream_op issues,
+    // so the difference to the futurized chain is the runtime alone
+    ofl::stream_launch(s->cs, sms, OFL_STREAM_TRIAD, a, b, c, 3.0, n);
     if (mode == 1) cudaEventRecord(ev, s->cs);
     if (mode == 2) cudaStreamSynchronize(s->cs);
   }

@@ -50,6 +50,10 @@ int cuda_error(cudaError_t e, const char* what);
 cudaError_t use_device(int dev);
 int num_sms(int dev);
 void count_launch(uint64_t n = 1);
+// the STREAM launcher behind ofl_stream_op (k_stream.cu), shared with the
+// raw-CUDA chain of the overhead benchmark so both launch identical kernels
+cudaError_t stream_launch(cudaStream_t st, int sms, int op, double* a, const double* b,
+                          const double* c, double scalar, uint64_t n);
 // cudaDeviceEnablePeerAccess(from -> to) once per pair, if the pair supports it
 void enable_peer(int from, int to);
 // Scratch of at least `bytes` on the stream's device (caller holds s->mu).
