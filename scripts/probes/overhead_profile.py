@@ -19,7 +19,7 @@ p.build("triad").get()
 payload = pinned_empty(8)
 args = [A, B, C, 3.0, n]
 grid, blk = (4, 1, 1), (256, 1, 1)
-K = 20000
+K = int(os.environ.get("K", 20000))
 
 
 def chain():
