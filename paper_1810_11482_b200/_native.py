@@ -142,6 +142,10 @@ EXPORTED = tuple(_SIGNATURES)
 
 _lib = None
 _lib_lock = threading.Lock()
+# csrc/oflcall.c: vectorcall entry points for the per-operation hot calls
+# (ofl_h2d, ofl_stream_op, ofl_wait), bound to the loaded library; None when the module
+# is not built (the ctypes prototypes then serve those calls too)
+_fast = None
 
 
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -162,8 +166,26 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
+            _bind_fast(lib)
             _lib = lib
     return _lib
+
+
+def _bind_fast(lib) -> None:
+    global _fast
+    try:
+        from . import _oflcall
+    except ImportError:
+        _fast = None
+        return
+    addr = lambda fn: ctypes.cast(fn, ctypes.c_void_p).value  # noqa: E731
+    _oflcall.bind(addr(lib.ofl_h2d), addr(lib.ofl_stream_op), addr(lib.ofl_wait))
+    _fast = _oflcall
+
+
+def fastcall():
+    """The bound _oflcall module (or None); call after load()."""
+    return _fast
 
 
 def last_error() -> str:

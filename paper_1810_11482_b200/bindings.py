@@ -24,7 +24,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from functools import lru_cache
 from typing import Callable, Optional
 
@@ -45,6 +45,12 @@ class Binding:
     launch: Callable
     # first out-of-bounds index (or None) given values and items
     oob: Optional[Callable] = None
+    # per parameter: 0 buffer, 1 scalar_f64, 2 scalar_u32 (the run fast path)
+    codes: tuple = field(default=(), init=False, compare=False)
+
+    def __post_init__(self):
+        object.__setattr__(self, "codes", tuple(0 if k.startswith("buffer") else (1 if k == "scalar_f64" else 2)
+                           for k in self.kinds))
 
 
 def _first_oob(candidates, failing) -> Optional[int]:
@@ -76,8 +82,17 @@ def _stream_binding(name: str, op: int, kinds: tuple) -> Binding:
         lo = min(v[0].size_bytes, v[1].size_bytes, v[2].size_bytes if has_c else 1 << 62) >> 3
         return lo if m > lo else None
 
+    fast = _native.fastcall()
+
     def launch(st, v, items, ticket):
         a, b, c, s, n = unpack(v)
+        if fast is not None:
+            t = fast.stream_op(st.ptr, op, a.ptr, b.ptr, c.ptr if c is not None else b.ptr,
+                               s, n if n < items else items)
+            if t < 0:
+                return -t
+            ticket.value = t
+            return 0
         return st.lib.ofl_stream_op(
             st.ptr, op, a.ptr, b.ptr, c.ptr if c is not None else b.ptr, s,
             n if n < items else items, ticket,

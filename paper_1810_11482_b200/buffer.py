@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes
 import threading
 
-from . import hostmem
+from . import _native, hostmem
 from .completion import DeviceToken
 from .device import DeviceObject
 from .errors import BadArgsError, OobAccessError
@@ -72,6 +72,14 @@ class BufferObject:
         ticket = _ticket_slot()
         dst = self.ptr + offset
         if n == 0 or type(owner) is hostmem.PinnedArray or hostmem.is_pinned(addr, n):
+            fast = _native._fast
+            if fast is not None:
+                t = fast.h2d(st.ptr, dst, addr, n)
+                if t < 0:
+                    raise_status(-t, "write")
+                if n:
+                    st.keep(t, owner)
+                return DeviceToken(st, t)
             status = lib.ofl_h2d(st.ptr, dst, addr, n, ctypes.byref(ticket))
             if status:
                 raise_status(status, "write")

@@ -188,7 +188,11 @@ class DeviceToken(CompletionToken):
                 if left <= 0:
                     return False
         s = self._stream
-        status = s.lib.ofl_wait(s.ptr, self._ticket)
+        fast = _native._fast
+        if fast is not None:
+            status = fast.wait(s.ptr, self._ticket)
+        else:
+            status = s.lib.ofl_wait(s.ptr, self._ticket)
         if status:
             self._fail(status, "device operation failed")
         else:

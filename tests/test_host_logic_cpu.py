@@ -115,3 +115,54 @@ def test_host_logic_against_null_abi(fake_lib):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "HOST-LOGIC OK" in r.stdout
+
+
+CALL_SRC = os.path.join(REPO, "paper_1810_11482_b200", "csrc", "oflcall.c")
+
+CALL_SCRIPT = textwrap.dedent(
+    r"""
+    import ctypes, importlib.util, sys
+    spec = importlib.util.spec_from_file_location("_oflcall", MOD_PATH)
+    m = importlib.util.module_from_spec(spec); spec.loader.exec_module(m)
+    lib = ctypes.CDLL(LIB_PATH)
+    addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value
+    try:
+        m.h2d(1, 2, 3, 4)
+        raise AssertionError("unbound call accepted")
+    except RuntimeError:
+        pass
+    m.bind(addr(lib.ofl_h2d), addr(lib.ofl_stream_op), addr(lib.ofl_wait))
+    s = ctypes.c_void_p()
+    assert lib.ofl_stream_create(0, ctypes.byref(s)) == 0
+    src = (ctypes.c_char * 8).from_buffer_copy(b"abcdefgh")
+    dst = (ctypes.c_char * 8)()
+    t1 = m.h2d(s.value, ctypes.addressof(dst), ctypes.addressof(src), 8)
+    assert bytes(dst) == b"abcdefgh" and t1 >= 1
+    t2 = m.stream_op(s.value, 3, 0, 0, 0, 3.0, 1024)
+    assert t2 == t1 + 1                      # tickets come back as the C side wrote them
+    assert m.h2d(0, 0, 0, 0) == -2           # a failing status comes back negated
+    assert m.stream_op(None, 3, 0, 0, 0, 3, 8) == -2
+    assert m.wait(s.value, t2) == 0
+    for bad in (lambda: m.h2d(1, 2, 3), lambda: m.h2d(-1, 0, 0, 0), lambda: m.stream_op(1, 3, 0, 0, 0, "x", 1)):
+        try:
+            bad()
+            raise AssertionError("bad call accepted")
+        except (TypeError, OverflowError):
+            pass
+    print("OFLCALL OK")
+    """
+)
+
+
+def test_oflcall_module_against_null_abi(fake_lib, tmp_path):
+    """csrc/oflcall.c (the vectorcall path for ofl_h2d / ofl_stream_op):
+    tickets and negated statuses round-trip, argument errors raise."""
+    import sysconfig
+
+    mod = str(tmp_path / ("_oflcall" + sysconfig.get_config_var("EXT_SUFFIX")))
+    subprocess.run(["gcc", "-O2", "-fPIC", "-shared", "-I" + sysconfig.get_paths()["include"],
+                    "-o", mod, CALL_SRC], check=True)
+    script = CALL_SCRIPT.replace("MOD_PATH", repr(mod)).replace("LIB_PATH", repr(fake_lib))
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OFLCALL OK" in r.stdout
