@@ -347,13 +347,20 @@ class MandelbrotTiles:
     """Config 3 on several devices: rows r with r mod G == g go to device g
     (cyclic split — contiguous bands leave devices idle); each
     device computes its rows packed densely.  A device's rows are computed in
-    ``chunks`` launches that alternate between two streams, and each chunk
-    is read with one strided DMA straight to its rows of the pinned host
-    image (``enqueue_read_rows_into``), so the read of chunk c overlaps the
-    computation of chunk c+1 and no host-side scatter copy is needed."""
+    ``chunks`` launches alternating over two compute streams (the tail of
+    one chunk overlaps the next); each chunk is read on a copy stream (which
+    waits, on the device, for that chunk's launch only) with one strided DMA straight to its rows of the pinned host image
+    (``enqueue_read_rows_into``), so the reads overlap the computation of the
+    later chunks and no host-side scatter copy is needed.
+
+    With ``interleave`` (default) chunk i of a device takes every chunks-th
+    of its rows starting at its i-th, so every chunk samples the whole image
+    and costs the same (bounded rows are far more expensive than escaping
+    ones); otherwise chunks are contiguous bands."""
 
     def __init__(self, devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
-                 viewport=VIEWPORT, esc: float = 4.0, stream: int = 0, chunks: int = 1):
+                 viewport=VIEWPORT, esc: float = 4.0, stream: int = 0, chunks: int = 1,
+                 interleave: bool = True):
         self.devices = list(devices)
         self.width, self.height, self.max_iter = width, height, max_iter
         self.viewport, self.esc = viewport, esc
@@ -361,31 +368,66 @@ class MandelbrotTiles:
         self.rows = [len(decomp.cyclic_rows(height, G, g)) for g in range(G)]
         self.progs = [_builtin(d, "mandelbrot_rows") for d in self.devices]
         self.streams, self.parts = [], []
+        self._reads = {}  # (device, chunk) -> ticket of the chunk's last read
         for g, d in enumerate(self.devices):
             r = self.rows[g]
             c = max(1, min(chunks, r))
-            self.streams.append([stream] if c == 1 else [d.create_stream(), d.create_stream()])
-            bounds = [r * i // c for i in range(c + 1)]
-            self.parts.append([(k0, k1, d.create_buffer(max(4, (k1 - k0) * width * 4)).get())
-                               for k0, k1 in zip(bounds, bounds[1:]) if k1 > k0])
+            # chunked: kernels alternate over two compute streams (the tail
+            # of one chunk overlaps the next), reads go on a third
+            self.streams.append([stream] if c == 1 else
+                                [d.create_stream(), d.create_stream(), d.create_stream()])
+            if interleave:
+                # (first device row, device-row step, rows)
+                spans = [(i, c, (r - i + c - 1) // c) for i in range(c)]
+            else:
+                bounds = [r * i // c for i in range(c + 1)]
+                spans = [(k0, 1, k1 - k0) for k0, k1 in zip(bounds, bounds[1:])]
+            self.parts.append([(k0, step, cnt, d.create_buffer(max(4, cnt * width * 4)).get())
+                               for k0, step, cnt in spans if cnt > 0])
         self.image = pinned_empty(width * height * 4, np.uint32)
 
     def enqueue(self) -> list:
         """Launch every chunk and its read into ``self.image``; returns the
         read tokens."""
+        from .. import _native
+        from ..completion import DeviceToken
+
         G = len(self.devices)
         re0, re1, im0, im1 = self.viewport
         w = self.width
         toks = []
         for g in range(G):
-            for i, (k0, k1, buf) in enumerate(self.parts[g]):
-                st = self.streams[g][i % len(self.streams[g])]
-                items = (g + (k1 - 1) * G + 1) * w  # through the chunk's last row
-                self.progs[g].run([buf, w, self.height, re0, re1, im0, im1, self.esc,
-                                   self.max_iter, g + k0 * G, G], "mandelbrot_rows",
-                                  (math.ceil(items / 256), 1, 1), (256, 1, 1), st)
-                toks.append(buf.enqueue_read_rows_into(0, self.image, w * 4, k1 - k0,
-                                                       (g + k0 * G) * w * 4, G * w * 4, st))
+            sids = self.streams[g]
+            copy = sids[-1]
+            split = len(sids) > 1
+            if split:
+                head = self.parts[g][0][3]
+                dev_obj = head._runtime.local._buffer(head.gid).device
+                s_copy = dev_obj.stream(copy)
+            for i, (k0, step, cnt, buf) in enumerate(self.parts[g]):
+                compute = sids[i % 2] if split else copy
+                if split:
+                    s_compute = dev_obj.stream(compute)
+                    prev = self._reads.get((g, i))
+                    if prev:  # WAR: the last read of this chunk's buffer
+                        _native.check(s_compute.lib.ofl_stream_wait(s_compute.ptr, s_copy.ptr,
+                                                                    prev), "chunk ordering")
+                first = g + k0 * G  # image row of the chunk's first row
+                items = (first + (cnt - 1) * step * G + 1) * w  # through its last row
+                run = self.progs[g].run([buf, w, self.height, re0, re1, im0, im1, self.esc,
+                                         self.max_iter, first, step * G], "mandelbrot_rows",
+                                        (items // w, 1, 1), (w, 1, 1), compute)  # exactly items
+                if split:
+                    if type(run) is not DeviceToken:
+                        run.get()  # a failed launch raises here
+                    # the copy stream waits for this chunk only (device-side)
+                    _native.check(s_copy.lib.ofl_stream_wait(s_copy.ptr, s_compute.ptr,
+                                                             run._ticket), "chunk ordering")
+                read = buf.enqueue_read_rows_into(0, self.image, w * 4, cnt, first * w * 4,
+                                                  step * G * w * 4, copy)
+                if split and type(read) is DeviceToken:
+                    self._reads[(g, i)] = read._ticket
+                toks.append(read)
         return toks
 
     def __call__(self, image: Optional[np.ndarray] = None) -> np.ndarray:
@@ -397,8 +439,10 @@ class MandelbrotTiles:
 
 
 def mandelbrot_multi(devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
-                     viewport=VIEWPORT, esc: float = 4.0, chunks: int = 1) -> np.ndarray:
-    return MandelbrotTiles(devices, width, height, max_iter, viewport, esc, chunks=chunks)()
+                     viewport=VIEWPORT, esc: float = 4.0, chunks: int = 1,
+                     interleave: bool = True) -> np.ndarray:
+    return MandelbrotTiles(devices, width, height, max_iter, viewport, esc, chunks=chunks,
+                           interleave=interleave)()
 
 
 # -- heat equation across devices (config 2) ---------------------------------------

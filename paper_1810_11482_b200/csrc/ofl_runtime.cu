@@ -394,8 +394,11 @@ int ofl_d2h_rows(ofl_stream* s, void* dst, uint64_t dst_pitch, const void* src,
   Enqueue q(s);
   if (!q.ok()) return q.status;
   if (row_bytes && rows) {
-    cudaError_t e = cudaMemcpy2DAsync(dst, dst_pitch, src, row_bytes, row_bytes, rows,
-                                      cudaMemcpyDeviceToHost, s->cs);
+    // contiguous rows: one linear DMA (a 2-D copy pays per row)
+    cudaError_t e = dst_pitch == row_bytes
+                        ? cudaMemcpyAsync(dst, src, row_bytes * rows, cudaMemcpyDeviceToHost, s->cs)
+                        : cudaMemcpy2DAsync(dst, dst_pitch, src, row_bytes, row_bytes, rows,
+                                            cudaMemcpyDeviceToHost, s->cs);
     if (e != cudaSuccess) return cuda_error(e, "cudaMemcpy2DAsync");
   }
   return q.finish(ticket);

@@ -453,18 +453,39 @@ def test_mandelbrot_cyclic_rows_two_devices(rt2):
     devices = rt2.get_all_devices().get()
     exp = oracle.mandelbrot(640, 360, max_iter=1000, threads=0).tobytes()
     for chunks in (1, 3, 8, 500):
-        counts = mandelbrot_multi(devices, 640, 360, 1000, chunks=chunks)
-        assert counts.tobytes() == exp, chunks
+        for interleave in (True, False):
+            counts = mandelbrot_multi(devices, 640, 360, 1000, chunks=chunks,
+                                      interleave=interleave)
+            assert counts.tobytes() == exp, (chunks, interleave)
 
 
-def test_mandelbrot_chunked_single_device_config3(dev, golden):
-    """Config 3 on one device in 8 chunks on two streams (read of chunk c
-    overlapping chunk c+1): the reference's sha256."""
+@pytest.mark.parametrize("w,h,bands", [(643, 357, 5), (640, 360, 1), (17, 9, 7), (1000, 3, 2),
+                                       (333, 101, 200)])
+def test_mandelbrot_chunked_ragged(dev, w, h, bands):
+    """Chunked (interleaved and banded) Mandelbrot into the pinned image on
+    ragged shapes (partial tiles, more chunks than rows): the image equals
+    the oracle's, and a second frame through the same streams is identical."""
+    from paper_1810_11482_b200.bench.harness import MandelbrotTiles
+
+    import oracle
+
+    exp = oracle.mandelbrot(w, h, max_iter=300, threads=0).tobytes()
+    for interleave in (True, False):
+        tiles = MandelbrotTiles([dev], w, h, 300, chunks=bands, interleave=interleave)
+        for _ in range(2):
+            tiles.image[:] = 0xFFFFFFFF
+            assert tiles().tobytes() == exp, interleave
+
+
+@pytest.mark.parametrize("chunks,interleave", [(8, True), (8, False), (16, True), (7, True)])
+def test_mandelbrot_chunked_single_device_config3(dev, golden, chunks, interleave):
+    """Config 3 on one device in chunks on two streams (read of chunk c
+    overlapping chunk c+1), interleaved or banded rows: the reference's sha256."""
     import hashlib
 
     from paper_1810_11482_b200.bench.harness import mandelbrot_multi
 
-    counts = mandelbrot_multi([dev], 7680, 4320, 2000, chunks=8)
+    counts = mandelbrot_multi([dev], 7680, 4320, 2000, chunks=chunks, interleave=interleave)
     assert hashlib.sha256(counts.tobytes()).hexdigest() == golden["mandelbrot"][7]["sha256"]
 
 
