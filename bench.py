@@ -213,9 +213,13 @@ def run_reference(args) -> None:
     el = time.perf_counter() - t0
     gbs = 24.0 * m * args.steps / el / 1e9
     r = {"gbs": gbs}
+    world = max(1, env_int("WORLD_SIZE", 1))
     sample = (f"{args.steps} timed triad sweeps (after {args.warmup} warm-up) over the first "
               f"{m} of N={n} fp64 elements ({el:.1f} s), C restatement in oracle/ on "
               f"{threads} host threads")
+    if world > 1:
+        sample += (f"; the whole job is {world} x N elements, all in the one host memory, so "
+                   "this bandwidth is the CPU path's rate for it")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -230,7 +234,7 @@ def run_reference(args) -> None:
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": workload_config(n, 1),
+        "config": workload_config(n, world),
         "cpu_baseline": {
             "value": round(r["gbs"], 3), "unit": "GB/s", "cores": threads, "kind": "port",
             "sample": sample,
