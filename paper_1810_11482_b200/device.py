@@ -75,7 +75,7 @@ class Stream:
     """One CUDA stream plus host objects that must outlive its in-flight
     operations (pinned sources, staging blocks)."""
 
-    __slots__ = ("ptr", "lib", "device", "sid", "_keep", "_purge_lock")
+    __slots__ = ("ptr", "lib", "device", "sid", "_keep", "_purge_lock", "err_slots")
 
     def __init__(self, device: "DeviceObject", sid: int):
         self.lib = _native.load()
@@ -86,6 +86,7 @@ class Stream:
         _native.check(self.lib.ofl_stream_create(device.ordinal, ctypes.byref(p)), "stream create")
         self.ptr = p.value
         self._keep: deque = deque()
+        self.err_slots = None  # jit._ErrSlots, created on the first NVRTC launch
 
     def done_ticket(self) -> int:
         return self.lib.ofl_stream_done(self.ptr)
@@ -140,12 +141,15 @@ class Stream:
 
     def destroy(self) -> None:
         if self.ptr:
-            self.lib.ofl_stream_destroy(self.ptr)
+            self.lib.ofl_stream_destroy(self.ptr)  # synchronises the stream first
             self.ptr = None
             while self._keep:
                 _, rel = self._keep.popleft()
                 if callable(rel):
                     rel()
+            slots, self.err_slots = self.err_slots, None
+            if slots is not None:
+                slots.free()
 
 
 class DeviceObject:

@@ -65,32 +65,41 @@ def compile_kernel(ir, ordinal: int):
 
 
 class _ErrSlots:
-    """Per-stream ring of 16-byte device error records."""
+    """Per-stream ring of 16-byte device error records, owned by the Stream
+    (freed in Stream.destroy).  Slots are taken under a lock: two threads
+    launching on one stream never share a record."""
 
-    __slots__ = ("base", "next")
+    __slots__ = ("device", "base", "next", "lock")
 
     def __init__(self, device):
+        self.device = device
         self.base = device.allocate(_SLOTS * 16)
         self.next = 0
+        self.lock = threading.Lock()
 
     def take(self) -> int:
-        k = self.next
-        self.next = (k + 1) % _SLOTS
+        with self.lock:
+            k = self.next
+            self.next = (k + 1) % _SLOTS
         return self.base + 16 * k
 
+    def free(self) -> None:
+        if self.base:
+            self.device.release(self.base, _SLOTS * 16)
+            self.base = 0
 
-_slots: dict = {}
+
 _slots_lock = threading.Lock()
 
 
 def _err_slot(stream) -> int:
-    s = _slots.get(stream.ptr)
+    s = stream.err_slots
     if s is None:
         with _slots_lock:
-            s = _slots.get(stream.ptr)
+            s = stream.err_slots
             if s is None:
                 s = _ErrSlots(stream.device)
-                _slots[stream.ptr] = s
+                stream.err_slots = s
     return s.take()
 
 

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 from typing import Optional, Sequence, Union
 
 from . import _native
@@ -238,25 +239,29 @@ class Runtime:
         raise UnknownGidError(f"{gid} names an unknown locality")
 
     def local_program(self, gid: GlobalId):
-        """(registry, generation, ProgramObject) for a program owned by this
-        process, else None — the handles' fast launch path (handles.py); the
-        resolution stays valid while ``registry.generation`` is unchanged."""
+        """(registry, generation, weakref to the ProgramObject) for a program
+        owned by this process, else None — the handles' fast launch path
+        (handles.py); the resolution stays valid while ``registry.generation``
+        is unchanged, and while it is the registry keeps the object alive, so
+        the weak reference resolves.  A weak reference, so that a handle's
+        cache never keeps an unregistered object's device memory alive."""
         if gid.locality_id != self.registry.self_locality_id:
             return None
         try:
             reg = self.registry
-            return reg, reg.generation, self.local._program(gid)
+            return reg, reg.generation, weakref.ref(self.local._program(gid))
         except Exception:  # noqa: BLE001 - the general path reports it
             return None
 
     def local_buffer(self, gid: GlobalId):
-        """(registry, generation, BufferObject) for a buffer owned by this
-        process, else None — the handles' fast paths (handles.py)."""
+        """(registry, generation, weakref to the BufferObject) for a buffer
+        owned by this process, else None — the handles' fast paths
+        (handles.py); see local_program for why the reference is weak."""
         if gid.locality_id != self.registry.self_locality_id:
             return None
         try:
             reg = self.registry
-            return reg, reg.generation, self.local._buffer(gid)
+            return reg, reg.generation, weakref.ref(self.local._buffer(gid))
         except Exception:  # noqa: BLE001 - the general path reports it
             return None
 

@@ -238,7 +238,97 @@ def fuzz_cases(dev, count: int = 150) -> list:
     return cases
 
 
+DOT_SEQ_SRC = """
+# fp32 dot product restated in the reference language (no f32 type,
+# lang.py:29): the f64 buffers hold fp32 values, so every product is exact
+# in f64 and work item 0 accumulates them in index order (pattern sum.k:3-11).
+kernel dot_seq(a : buffer_f64, b : buffer_f64, res : buffer_f64, n : scalar_u32) {
+    if (gtid == 0) {
+        let acc = 0.0;
+        for i in 0 .. n {
+            acc = acc + a[i] * b[i];
+        }
+        res[0] = acc;
+    }
+}
+"""
+
+# (n, seed): BASELINE config 4 inputs are rng(seed).random(n, float32) for a,
+# then b; the full 2^31 is beyond the reference's 8-GiB-per-buffer host path,
+# so the reference runs prefixes of the same generator family.
+DOT_CASES = ((1 << 24, 20180214), ((1 << 24) + 3, 611), (1 << 26, 20180214))
+
+# (n, steps, seed): config 2 (2^28 x 1000, the reference's stencil.k
+# iterated ping-pong, harness.py:199-230 inputs) and a 2^20 x 1000 case.
+HEAT_LONG = ((1 << 20, 1000, 20180214), (1 << 28, 1000, 20180214))
+
+
+def dot_long(dev) -> list:
+    cases = []
+    for n, seed in DOT_CASES:
+        rng = np.random.default_rng(seed)
+        a = rng.random(n, dtype=np.float32)
+        b = rng.random(n, dtype=np.float32)
+        ab = buf_with(dev, a.astype(np.float64).tobytes())
+        bb = buf_with(dev, b.astype(np.float64).tobytes())
+        rb = dev.create_buffer(8).get()
+        t1 = time.time()
+        run(dev, DOT_SEQ_SRC, "dot_seq", [ab, bb, rb, n], 32, 32)
+        res = float(np.frombuffer(rb.enqueue_read_sync(0, 8), np.float64)[0])
+        cases.append({"n": n, "seed": seed, "result": res, "result_hex": float.hex(res),
+                      "reference_seconds": round(time.time() - t1, 2)})
+        print("dot", cases[-1], flush=True)
+    return cases
+
+
+def heat_long(dev, only_small: bool = False) -> list:
+    cases = []
+    for n, steps, seed in HEAT_LONG:
+        if only_small and n > (1 << 20):
+            continue
+        x = np.random.default_rng(seed).random(n)
+        a, b = buf_with(dev, x.tobytes()), dev.create_buffer(n * 8).get()
+        del x
+        prog = dev.create_program_with_source(kernel_source("stencil")).get()
+        prog.build("stencil").get(timeout=600)
+        grid = (math.ceil(n / 256), 1, 1)
+        t1 = time.time()
+        for s in range(steps):
+            src, dst = (a, b) if s % 2 == 0 else (b, a)
+            prog.run([src, dst, n], "stencil", grid, (256, 1, 1)).get(timeout=3600)
+            if s % 50 == 0:
+                print(f"heat n={n} step {s} {time.time() - t1:.1f}s", flush=True)
+        final = a if steps % 2 == 0 else b
+        raw = final.enqueue_read_sync(0, n * 8)
+        vals = np.frombuffer(raw, np.float64)
+        cases.append({"n": n, "steps": steps, "seed": seed, "sha256": sha(raw),
+                      "sum": float(vals.sum()), "max": float(vals.max()),
+                      "reference_seconds": round(time.time() - t1, 1)})
+        print("heat", cases[-1], flush=True)
+        del raw, vals
+    return cases
+
+
+def long_main() -> None:
+    """--long: reference outputs for config 2 (full 2^28 x 1000 heat, ~20 min
+    on the host backend) and config 4 (sequential fp64 dot of fp32 values),
+    written to golden_long.json."""
+    path = os.path.join(HERE, "golden_long.json")
+    out = {"generator": "tests/golden/make_golden.py --long",
+           "reference": "offloadrt (host backend)"}
+    small = "--small" in sys.argv
+    with Runtime(backend="host") as rt:
+        dev = rt.get_all_devices().get()[0]
+        out["dot"] = dot_long(dev)
+        out["heat"] = heat_long(dev, only_small=small)
+    with open(path, "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(f"wrote {path}")
+
+
 def main() -> None:
+    if "--long" in sys.argv:
+        return long_main()
     if "--only-fuzz" in sys.argv:  # add/refresh the fuzz section in place
         path = os.path.join(HERE, "golden.json")
         with open(path) as fh:

@@ -508,3 +508,27 @@ def test_nccl_allreduce_single_rank(dev, rt):
     buf.enqueue_write(0, np.array([2.5]).tobytes())
     comm.allreduce([buf], count=1, dtype="f64").get()
     assert np.frombuffer(buf.enqueue_read_sync(0, 8), np.float64)[0] == 2.5
+
+
+def test_when_all_runs_read_landing(dev):
+    """A pageable enqueue_read_into lands through a staging block in its
+    token's finish step: gating on when_all(...).get() / then() / done() must
+    make the bytes visible (reference futures.py:189-216)."""
+    n = 3 << 20
+    payload = np.random.default_rng(5).integers(0, 256, n, dtype=np.uint8)
+    buf = dev.create_buffer(n).get()
+    buf.enqueue_write(0, payload)
+    out = bytearray(n)
+    assert when_all([buf.enqueue_read_into(0, out)]).get(timeout=30) is None
+    assert bytes(out) == payload.tobytes()
+    out2 = bytearray(n)
+    seen, fired = [], threading.Event()
+    when_all([buf.enqueue_read_into(0, out2), buf.enqueue_write(0, payload)]).then(
+        lambda _: (seen.append(bytes(out2) == payload.tobytes()), fired.set()))
+    assert fired.wait(30) and seen == [True]
+    out3 = np.zeros(n, np.uint8)
+    agg = when_all([buf.enqueue_read_into(0, out3)])
+    t0 = time.time()
+    while not agg.done():
+        assert time.time() - t0 < 30
+    assert out3.tobytes() == payload.tobytes()

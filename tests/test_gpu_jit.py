@@ -105,3 +105,32 @@ def test_fuzzed_kernels_match_reference(dev, golden):
         if err != case["error"] or outs != case["outputs_hex"]:
             failures.append((i, err, case["error"], case["source"]))
     assert not failures, f"{len(failures)} of {len(golden['fuzz'])} differ; first: {failures[0]}"
+
+
+def test_jit_abort_fails_when_all_and_then(dev):
+    """An NVRTC kernel's abort is found by its token's finish step (the error
+    record read back); when_all and then() over the aggregate must run it and
+    fail with the same error (reference futures.py:189-216)."""
+    import threading
+
+    from paper_1810_11482_b200 import when_all
+
+    src = "kernel o(out : buffer_f64, n : scalar_u32) { out[gtid * 3] = 1.0; }"
+    p = dev.create_program_with_source(src).get()
+    p.build("o").get(timeout=120)
+    buf = dev.create_buffer(100 * 8).get()
+    msg = "kernel buffer index 102 out of range"
+    with pytest.raises(OobAccessError, match=msg):
+        when_all([buf.enqueue_write(0, b"\0" * 8), p.run([buf, 0], "o", (4, 1, 1), (256, 1, 1))]).get()
+    with pytest.raises(OobAccessError, match=msg):
+        when_all([when_all([p.run([buf, 0], "o", (4, 1, 1), (256, 1, 1))])]).get(timeout=30)
+    seen, fired = [], threading.Event()
+    agg = when_all([p.run([buf, 0], "o", (4, 1, 1), (256, 1, 1))])
+    agg.then(lambda _: seen.append("ran")).then(lambda _: None)._on_done(
+        lambda t: (seen.append(str(t.error())), fired.set()))
+    assert fired.wait(30)
+    assert seen and msg in seen[-1] and "ran" not in seen
+    tok = p.run([buf, 0], "o", (4, 1, 1), (256, 1, 1))
+    while not when_all([tok]).done():
+        pass
+    assert when_all([tok]).is_failed() and msg in str(tok.error())

@@ -95,6 +95,50 @@ SCRIPT = textwrap.dedent(
         assert fired, "continuation never fired"
         assert d0.synchronize().get() is None
 
+        # when_all runs every input's finish step and fails with its error
+        # (reference futures.py:189-216; pkg/tests/test_futures.py:104-113)
+        from paper_1810_11482_b200.completion import DeviceToken
+        buf.enqueue_write(0, bytes(range(64)))
+        big = d0.create_buffer(1 << 20).get()
+        payload = np.random.default_rng(1).integers(0, 256, 1 << 20, dtype=np.uint8)
+        big.enqueue_write(0, payload)
+        out = bytearray(1 << 20)                       # pageable: lands via staging
+        assert when_all([big.enqueue_read_into(0, out)]).get() is None
+        assert bytes(out) == payload.tobytes(), "read_into not visible after when_all.get()"
+        out2 = bytearray(1 << 20)
+        seen = []
+        agg = when_all([make_ready(), when_all([big.enqueue_read_into(0, out2)])])
+        agg.then(lambda _: seen.append(bytes(out2) == payload.tobytes()))
+        t0 = time.time()
+        while not seen and time.time() - t0 < 5:
+            time.sleep(0.01)
+        assert seen == [True], f"then() on the aggregate ran before the landing: {seen}"
+        out3 = bytearray(16)
+        r = big.enqueue_read_into(0, out3)
+        assert when_all([r]).done() and bytes(out3) == payload[:16].tobytes()
+        st = rt.local._device(d0.gid).stream(0)
+        tk = st.tail()
+        def boom():
+            raise OobAccessError("kernel buffer index 7 out of range")
+        bad = DeviceToken(st, tk, boom)
+        try:
+            when_all([buf.enqueue_write(0, b"x"), bad, buf.enqueue_write(0, b"y")]).get()
+        except OobAccessError as e:
+            assert "index 7" in str(e)
+        else:
+            raise AssertionError("finish error swallowed by when_all")
+        assert bad.is_failed() and "index 7" in str(bad.error())
+        bad2 = DeviceToken(st, tk, boom)
+        got = []
+        when_all([bad2]).then(lambda _: got.append("ok")).then(
+            lambda _: None)._on_done(lambda t: got.append(type(t.error()).__name__))
+        t0 = time.time()
+        while not got and time.time() - t0 < 5:
+            time.sleep(0.01)
+        assert got == ["OobAccessError"], got
+        bad3 = DeviceToken(st, tk, boom)
+        assert when_all([when_all([bad3])]).is_failed()
+
         rt.registry.unregister(buf.gid)
         raises(UnknownGidError, lambda: buf.enqueue_read(0, 1).get())
     print("HOST-LOGIC OK")
