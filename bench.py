@@ -70,7 +70,7 @@ def ncu_traffic() -> dict:
 class ClockSampler:
     """nvidia-smi-equivalent sampling (NVML) during the timed region."""
 
-    def __init__(self, index: int, period: float = 0.01):
+    def __init__(self, index: int, period: float = 0.002):
         self.samples: list = []
         self.reasons: set = set()
         self.max_mhz = None
@@ -93,21 +93,24 @@ class ClockSampler:
         0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
     }
 
-    def _run(self):
+    def _sample(self):
         nv = self._nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self._REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
-            self._stop.wait(self.period)
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            for bit, name in self._REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _run(self):
+        while not self._stop.wait(self.period):
+            self._sample()
 
     def start(self):
         if self._nv is not None:
+            self._sample()  # at least one sample inside even a short region
             self._thread = threading.Thread(target=self._run, daemon=True)
             self._thread.start()
 
@@ -153,6 +156,13 @@ class Dist:
         t = self.torch.tensor([x], dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
+
+    def gather(self, obj) -> list:
+        if self.dist is None:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
 
     def close(self):
         if self.dist is not None:
@@ -256,54 +266,60 @@ def workload_config(n: int, world: int) -> dict:
     }
 
 
-def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int, payload_bytes: int = 8) -> dict:
-    """Per-future overhead vs raw CUDA streams (BASELINE config 5)."""
-    import numpy as np
+class OverheadBench:
+    """Per-future overhead vs raw CUDA streams (BASELINE config 5).
 
-    from paper_1810_11482_b200 import _native, make_ready, pinned_empty, when_all
-    from paper_1810_11482_b200.bindings import kernel_source
+    One step = an 8-byte H2D write + the STREAM triad over N=1024 (the
+    product kernel and launch), chained K deep.  Futurized: every step is
+    ``w = enqueue_write; r = run; prev = when_all([prev, w, r])`` and the
+    chain ends with ``prev.get()``.  Raw (csrc/ofl_bench.cu, a C loop on the
+    CUDA runtime): the same cudaMemcpyAsync + launch per step, mode 0 =
+    stream order only, mode 1 = an event recorded after each step and waited
+    on by the next (explicit dependency chaining); cudaStreamSynchronize at
+    the end.  BASELINE.md §3: overhead per future = (t_futurized - t_raw)/K,
+    one future per step (the step's when_all), no other division.  Each K
+    is timed as the min over 3 batches of the mean time per chain, a batch
+    holding enough chains to last >= ~20 ms.  Sync-each-step: ``run().get()``
+    every step vs raw mode 2 (cudaStreamSynchronize per step)."""
 
-    lib = _native.load()
-    n = 1024
-    A, B, C, D = (dev.create_buffer(n * 8).get() for _ in range(4))
-    prog = dev.create_program_with_source(kernel_source("stream")).get()
-    prog.build("triad").get()
-    payload = pinned_empty(payload_bytes)
-    payload[:] = 1
-    args = [A, B, C, 3.0, n]
-    grid, block = ((n + 255) // 256, 1, 1), (256, 1, 1)
-    stream = rt.device_objects()[0].stream(0)
-    dptr = rt.local._buffer(D.gid).ptr
-    aptr, bptr, cptr = (rt.local._buffer(x.gid).ptr for x in (A, B, C))
+    def __init__(self, dev, rt, payload_bytes: int = 8):
+        import numpy as np
 
-    def raw(steps: int, mode: int) -> float:
+        from paper_1810_11482_b200 import _native, pinned_empty
+        from paper_1810_11482_b200.bindings import kernel_source
+
+        self.lib = _native.load()
+        self._native = _native
+        self.dev = dev
+        self.n = n = 1024
+        self.A, self.B, self.C, self.D = (dev.create_buffer(n * 8).get() for _ in range(4))
+        self.prog = dev.create_program_with_source(kernel_source("stream")).get()
+        self.prog.build("triad").get()
+        self.payload_bytes = payload_bytes
+        self.payload = pinned_empty(payload_bytes)
+        self.payload[:] = 1
+        self.args = [self.A, self.B, self.C, 3.0, n]
+        self.grid, self.block = ((n + 255) // 256, 1, 1), (256, 1, 1)
+        self.stream = rt.device_objects()[0].stream(0)
+        self.dptr = rt.local._buffer(self.D.gid).ptr
+        self.ptrs = [rt.local._buffer(x.gid).ptr for x in (self.A, self.B, self.C)]
+        del np
+
+    def raw(self, steps: int, mode: int) -> float:
         secs = ctypes.c_double()
-        _native.check(
-            lib.ofl_bench_raw_chain(
-                stream.ptr, dptr, payload.ctypes.data, payload_bytes, aptr, bptr, cptr, n, steps,
-                mode,
-                ctypes.byref(secs),
-            ),
-            "raw chain",
-        )
+        a, b, c = self.ptrs
+        self._native.check(
+            self.lib.ofl_bench_raw_chain(self.stream.ptr, self.dptr, self.payload.ctypes.data,
+                                         self.payload_bytes, a, b, c, self.n, steps, mode,
+                                         ctypes.byref(secs)),
+            "raw chain")
         return secs.value
 
-    def capi(steps: int) -> float:
-        # the product C-ABI (libofl tickets, same kernel launch) called from
-        # Python without futures: splits the overhead into C-ABI + futures
-        t = ctypes.c_uint64()
-        ref = ctypes.byref(t)
-        h2d, op, sp, src = lib.ofl_h2d, lib.ofl_stream_op, stream.ptr, payload.ctypes.data
-        dev.synchronize().get()
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            h2d(sp, dptr, src, payload_bytes, ref)
-            op(sp, 3, aptr, bptr, cptr, 3.0, n, ref)
-        dev.synchronize().get()
-        return time.perf_counter() - t0
+    def futurized(self, steps: int) -> float:
+        from paper_1810_11482_b200 import make_ready, when_all
 
-    def pipelined(steps: int) -> float:
-        dev.synchronize().get()
+        D, prog, args, grid, block, payload = (self.D, self.prog, self.args, self.grid,
+                                               self.block, self.payload)
         t0 = time.perf_counter()
         prev = make_ready(None)
         for _ in range(steps):
@@ -313,44 +329,289 @@ def overhead_sweep(dev, rt, steps_pipelined: int, steps_sync: int, payload_bytes
         prev.get()
         return time.perf_counter() - t0
 
-    def synced(steps: int) -> float:
-        dev.synchronize().get()
+    def synced(self, steps: int) -> float:
+        D, prog, args, grid, block, payload = (self.D, self.prog, self.args, self.grid,
+                                               self.block, self.payload)
         t0 = time.perf_counter()
         for _ in range(steps):
             D.enqueue_write(0, payload)
             prog.run(args, "triad", grid, block).get()
         return time.perf_counter() - t0
 
-    # warm both paths
-    raw(200, 0)
-    capi(200)
-    pipelined(200)
-    raw(100, 2)
-    synced(100)
+    @staticmethod
+    def per_chain(fn, k: int) -> float:
+        """min over 3 batches of the mean seconds per K-step chain."""
+        reps = max(1, 2000 // k)
+        best = float("inf")
+        for _ in range(3):
+            t = sum(fn(k) for _ in range(reps)) / reps
+            best = min(best, t)
+        return best
+
+    def point(self, k: int) -> dict:
+        self.dev.synchronize().get()
+        raw0 = self.per_chain(lambda s: self.raw(s, 0), k)
+        raw1 = self.per_chain(lambda s: self.raw(s, 1), k)
+        fut = self.per_chain(self.futurized, k)
+        us = 1e6 / k
+        return {
+            "K": k,
+            "raw_stream_order_us_per_step": round(raw0 * us, 3),
+            "raw_event_chained_us_per_step": round(raw1 * us, 3),
+            "futurized_us_per_step": round(fut * us, 3),
+            "overhead_us_per_future": round((fut - raw0) * us, 3),
+            "overhead_us_per_future_vs_event_chained": round((fut - raw1) * us, 3),
+        }
+
+    def sync_point(self, k: int) -> dict:
+        self.dev.synchronize().get()
+        raw2 = self.per_chain(lambda s: self.raw(s, 2), k)
+        fut = self.per_chain(self.synced, k)
+        us = 1e6 / k
+        return {"K": k, "raw_sync_each_step_us": round(raw2 * us, 3),
+                "futurized_get_each_step_us": round(fut * us, 3),
+                "overhead_us_per_future": round((fut - raw2) * us, 3)}
+
+    def sweep(self, ks=(1, 10, 100, 1000, 10000, 100000), sync_k: int = 1000) -> dict:
+        # warm both paths (first launches, pinned-range lookups, JIT-free)
+        self.raw(200, 0)
+        self.raw(200, 1)
+        self.futurized(200)
+        self.synced(50)
+        points = [self.point(k) for k in ks]
+        head = next((p for p in points if p["K"] == 10000), points[-1])
+        return {
+            "formula": "(t_futurized - t_raw) / K per K-step chain, one future per step "
+                       "(BASELINE.md §3); raw = same cudaMemcpyAsync + launch from C",
+            "step": f"H2D {self.payload_bytes} B + triad N={self.n}, prev = when_all([prev, w, r])",
+            "overhead_us_per_future": head["overhead_us_per_future"],
+            "overhead_us_per_future_vs_event_chained":
+                head["overhead_us_per_future_vs_event_chained"],
+            "at_K": head["K"],
+            "max_over_K_us": max(p["overhead_us_per_future"] for p in points),
+            "sweep": points,
+            "sync_each_step": self.sync_point(sync_k),
+            "target_us": 5.0,
+        }
+
+
+class EventTimer:
+    """CUDA events on one stream (libofl events): device time of what is
+    enqueued between start() and stop()."""
+
+    def __init__(self, lib, stream, ordinal: int):
+        from paper_1810_11482_b200 import _native
+
+        self.lib, self.stream, self._native = lib, stream, _native
+        self.a, self.b = ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(lib.ofl_event_create(ordinal, ctypes.byref(self.a)), "event")
+        _native.check(lib.ofl_event_create(ordinal, ctypes.byref(self.b)), "event")
+
+    def start(self):
+        self.lib.ofl_event_record(self.a, self.stream.ptr)
+
+    def stop(self) -> float:
+        self.lib.ofl_event_record(self.b, self.stream.ptr)
+        ms = ctypes.c_float()
+        self._native.check(self.lib.ofl_event_elapsed_ms(self.a, self.b, ctypes.byref(ms)),
+                           "elapsed")
+        return ms.value
+
+
+def _golden(name: str) -> dict:
+    try:
+        with open(os.path.join(REPO, "tests", "golden", name)) as fh:
+            return json.load(fh)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def _sha(buf) -> str:
+    import hashlib
+
+    return hashlib.sha256(memoryview(buf).cast("B")).hexdigest()
+
+
+def fp64_peak_ops(lib, stream) -> float:
+    """Measured FP64 DMUL/DADD issue rate (ops/s), csrc/ofl_bench.cu."""
+    v = ctypes.c_double()
+    if lib.ofl_bench_fp64_peak(stream.ptr, ctypes.byref(v)):
+        return 0.0
+    return v.value
+
+
+def config_heat(rt, dev, lib, fp64: float, n: int = 1 << 28, steps: int = 1000) -> dict:
+    """Config 2 on one GPU: 2^28 cells x 1000 steps of stencil.k through the
+    `heat` builtin; parity = sha256 of the final field equals the REFERENCE's
+    (tests/golden/golden_long.json, offloadrt host backend, ~13 min)."""
+    import numpy as np
+
+    from paper_1810_11482_b200 import pinned_empty
+
+    st = rt.device_objects()[0].stream(0)
+    x = pinned_empty(n * 8, np.float64)
+    x[:] = np.random.default_rng(20180214).random(n)
+    xout = pinned_empty(n * 8, np.float64)
+    X, Y = dev.create_buffer(n * 8).get(), dev.create_buffer(n * 8).get()
+    prog = dev.create_builtin_program().get()
+    prog.build("heat").get()
+    final = X if steps % 2 == 0 else Y
+    grid, block = (n // 256, 1, 1), (256, 1, 1)
+    e2e = []
+    for _ in range(3):  # end to end: pinned x in, 1000 steps, field back out
+        dev.synchronize().get()
+        t0 = time.perf_counter()
+        X.enqueue_write(0, x)
+        prog.run([X, Y, n, steps], "heat", grid, block)
+        final.enqueue_read_into(0, xout).get()
+        e2e.append(time.perf_counter() - t0)
+    ref = next((c for c in _golden("golden_long.json").get("heat", [])
+                if c["n"] == n and c["steps"] == steps), None)
+    digest = _sha(xout)
+    kernel = []
+    for _ in range(3):  # device time of the steps alone (input re-written, untimed)
+        X.enqueue_write(0, x)
+        t = EventTimer(lib, st, dev_ordinal(rt))
+        t.start()
+        prog.run([X, Y, n, steps], "heat", grid, block)
+        kernel.append(t.stop())
+    ms = min(kernel)
+    useful = 2.0 * n * steps  # 2 FP64 ops per cell-step (the fused update; reference: 2 mul + 2 add)
+    alg_bytes = 16.0 * n * steps
+    return {
+        "workload": "heat 2^28 fp64 x 1000 steps (BASELINE config 2), builtin `heat`, 1 GPU",
+        "kernel_ms": round(ms, 3),
+        "effective_gbs": round(alg_bytes / (ms * 1e-3) / 1e9, 1),
+        "useful_fp64_ops_per_s": round(useful / (ms * 1e-3), 1),
+        "fp64_peak_ops_per_s": round(fp64, 1),
+        "frac_fp64": round(useful / (ms * 1e-3) / fp64, 4) if fp64 else None,
+        "e2e_ms_pinned_host": round(min(e2e) * 1e3, 2),
+        "e2e_h2d_bytes": n * 8, "e2e_d2h_bytes": n * 8,
+        "sha256": digest,
+        "parity": ("bit-exact vs reference (golden_long.json)" if ref and digest == ref["sha256"]
+                   else "MISMATCH vs reference" if ref else "reference sha unavailable"),
+        "note": "effective_gbs counts 16 B/cell/step; temporal blocking keeps tb steps "
+                "in registers, so it exceeds the HBM roofline and FP64 issue is the bound",
+    }
+
+
+def config_mandelbrot(rt, dev, lib, fp64: float) -> dict:
+    """Config 3: 7680x4320, max_iter 2000, the reference's mandelbrot.k;
+    parity = sha256 of the counts equals the reference's (golden.json)."""
+    import numpy as np
+
+    from paper_1810_11482_b200 import pinned_empty, when_all
+    from paper_1810_11482_b200.bench.harness import MandelbrotTiles
+    from paper_1810_11482_b200.bindings import kernel_source
+
+    w, h, it = 7680, 4320, 2000
+    st = rt.device_objects()[0].stream(0)
+    O = dev.create_buffer(w * h * 4).get()
+    prog = dev.create_program_with_source(kernel_source("mandelbrot")).get()
+    prog.build("mandelbrot").get()
+    args = [O, w, h, -2.0, 1.0, -1.5, 1.5, 4.0, it]
+    grid = ((w * h + 255) // 256, 1, 1)
+    for _ in range(3):
+        prog.run(args, "mandelbrot", grid, (256, 1, 1))
+    t = EventTimer(lib, st, dev_ordinal(rt))
+    K = 10
+    t.start()
+    for _ in range(K):
+        prog.run(args, "mandelbrot", grid, (256, 1, 1))
+    ms = t.stop() / K
+    host = pinned_empty(w * h * 4, np.uint32)
+    O.enqueue_read_into(0, host).get()
+    ref = next((c for c in _golden("golden.json").get("mandelbrot", [])
+                if c["width"] == w and c["height"] == h and c["max_iter"] == it), None)
+    ok = ref is not None and _sha(host) == ref["sha256"]
+    total = int(host.astype(np.uint64).sum())
+    escaped = int((host < it).sum())
+    dp_ops = 8 * total + 3 * escaped  # the reference's evaluation, per counted iteration
+    tiles = MandelbrotTiles([dev], w, h, it, chunks=8)
+    when_all(tiles.enqueue()).get()
+    e2e = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        when_all(tiles.enqueue()).get()
+        e2e.append(time.perf_counter() - t0)
+    ok_e2e = ref is not None and _sha(tiles.image) == ref["sha256"]
+    return {
+        "workload": "Mandelbrot 7680x4320 max_iter 2000 (BASELINE config 3), 1 GPU",
+        "kernel_ms": round(ms, 3),
+        "e2e_ms_overlapped_into_pinned_image": round(min(e2e) * 1e3, 3),
+        "e2e_d2h_bytes": w * h * 4,
+        "reference_dp_ops": dp_ops,
+        "reference_op_rate_over_fp64_peak": round(dp_ops / (ms * 1e-3) / fp64, 4) if fp64 else None,
+        "note": "exact cycle detection stops provably periodic orbits early, so the "
+                "reference-op rate is an equivalent rate and may exceed 1",
+        "parity": "bit-exact vs reference sha256 (kernel and overlapped e2e)" if ok and ok_e2e
+                  else "MISMATCH vs reference",
+    }
+
+
+def config_dot(rt, dev, lib, n: int = 1 << 31) -> dict:
+    """Config 4 on one GPU: fp32 dot over 2^31 elements, fp64 accumulation;
+    parity = relative error vs the fp64 oracle (tolerance 1e-5)."""
+    import numpy as np
+
+    import oracle
+
+    st = rt.device_objects()[0].stream(0)
+    rng = np.random.default_rng(20180214)
+    a = rng.random(n, dtype=np.float32)
+    b = rng.random(n, dtype=np.float32)
+    A, B, R = dev.create_buffer(n * 4).get(), dev.create_buffer(n * 4).get(), dev.create_buffer(8).get()
+    prog = dev.create_builtin_program().get()
+    prog.build("dot_f32").get()
+    grid = (n // 256, 1, 1)
+    e2e = []
+    for _ in range(2):  # end to end from the pageable numpy arrays
+        dev.synchronize().get()
+        t0 = time.perf_counter()
+        A.enqueue_write(0, a)
+        B.enqueue_write(0, b)
+        prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
+        got = float(np.frombuffer(R.enqueue_read(0, 8).get(), np.float64)[0])
+        e2e.append(time.perf_counter() - t0)
+    t = EventTimer(lib, st, dev_ordinal(rt))
+    K = 10
+    t.start()
+    for _ in range(K):
+        prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
+    ms = t.stop() / K
+    exp = oracle.dot_f32(a, b, threads=0)
+    rel = abs(got - exp) / abs(exp)
+    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+    peak, _ = hbm_peak()
+    return {
+        "workload": "dot fp32 N=2^31, fp64 accumulation (BASELINE config 4), 1 GPU",
+        "kernel_ms": round(ms, 3), "gbs": round(gbs, 1), "frac_hbm": round(gbs / peak, 4),
+        "e2e_ms_pageable_numpy": round(min(e2e) * 1e3, 1), "e2e_h2d_bytes": 8 * n,
+        "rel_err_vs_oracle": rel,
+        "parity": "within 1e-12 (tolerance 1e-5) of the fp64 oracle" if rel <= 1e-12
+                  else ("within 1e-5" if rel <= 1e-5 else "MISMATCH"),
+    }
+
+
+def dev_ordinal(rt) -> int:
+    return rt.device_objects()[0].ordinal
+
+
+def run_configs(rt, dev, lib, names) -> dict:
     out = {}
-    t_raw = min(raw(steps_pipelined, 0) for _ in range(3))
-    t_capi = min(capi(steps_pipelined) for _ in range(3))
-    t_fut = min(pipelined(steps_pipelined) for _ in range(3))
-    out["pipelined_when_all"] = {
-        "steps": steps_pipelined,
-        "raw_us_per_step": t_raw / steps_pipelined * 1e6,
-        "c_abi_us_per_step": t_capi / steps_pipelined * 1e6,
-        "futurized_us_per_step": t_fut / steps_pipelined * 1e6,
-        "overhead_us_per_step": (t_fut - t_raw) / steps_pipelined * 1e6,
-        "overhead_us_per_future": (t_fut - t_raw) / steps_pipelined / 2 * 1e6,
-    }
-    t_raw = min(raw(steps_sync, 2) for _ in range(3))
-    t_fut = min(synced(steps_sync) for _ in range(3))
-    out["sync_each_step"] = {
-        "steps": steps_sync,
-        "raw_us_per_step": t_raw / steps_sync * 1e6,
-        "futurized_us_per_step": t_fut / steps_sync * 1e6,
-        "overhead_us_per_step": (t_fut - t_raw) / steps_sync * 1e6,
-    }
-    for v in out.values():
-        for k in list(v):
-            if isinstance(v[k], float):
-                v[k] = round(v[k], 3)
+    st = rt.device_objects()[0].stream(0)
+    fp64 = fp64_peak_ops(lib, st)
+    for name in names:
+        t0 = time.time()
+        fn = {"heat": lambda: config_heat(rt, dev, lib, fp64),
+              "mandelbrot": lambda: config_mandelbrot(rt, dev, lib, fp64),
+              "dot": lambda: config_dot(rt, dev, lib)}[name]
+        try:
+            out[name] = fn()
+        except Exception as exc:  # noqa: BLE001 - reported, the headline still prints
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        out[name]["wall_s"] = round(time.time() - t0, 1)
+        dev.synchronize().get()
     return out
 
 
@@ -419,6 +680,12 @@ def run_ours(args) -> None:
     total_ms = ms.value
     dist.barrier()
     job_ms = dist.max(total_ms)
+    clocks_per_rank = dist.gather(dict(clocks, rank=rank, ordinal=ordinal, device_ms=total_ms))
+    if world > 1:
+        # the job's clock summary: the slowest rank's median, all reasons seen
+        meds = [c["sm_mhz"] for c in clocks_per_rank if c.get("sm_mhz")]
+        clocks = dict(clocks, sm_mhz=min(meds) if meds else clocks.get("sm_mhz"),
+                      reasons=sorted({r for c in clocks_per_rank for r in c.get("reasons", [])}))
 
     step_bytes = 24 * n
     value = world * step_bytes * args.steps / (job_ms * 1e-3) / 1e9
@@ -461,7 +728,13 @@ def run_ours(args) -> None:
 
     overhead = None
     if rank == 0 and not args.no_overhead:
-        overhead = overhead_sweep(dev, rt, args.overhead_steps, max(100, args.overhead_steps // 10))
+        ks = tuple(int(k) for k in args.overhead_ks.split(",") if k)
+        overhead = OverheadBench(dev, rt).sweep(ks)
+
+    configs = None
+    if rank == 0 and world == 1 and args.configs:
+        configs = run_configs(rt, dev, lib, [c for c in args.configs.split(",") if c])
+        configs["overhead"] = overhead
 
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
@@ -515,7 +788,9 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "clocks_per_rank": clocks_per_rank if world > 1 else None,
             "future_overhead_us": overhead,
+            "configs": configs,
             "parity": "bit-exact vs CPU oracle (oracle/ofl_oracle.c)",
             "oversubscribed": oversubscribed,
         }
@@ -524,24 +799,73 @@ def run_ours(args) -> None:
     dist.close()
 
 
+# Build-time / sweep switches that change which kernel variant runs; a
+# headline number must come from the shipped defaults.
+VARIANT_SWITCHES = ("OFL_HEAT_TB", "OFL_HEAT_R", "OFL_HEAT_FMA", "OFL_HEAT_KERNEL",
+                    "OFL_MANDEL_PERIOD", "OFL_MANDEL_FPCMP", "OFL_MANDEL_FUSED", "OFL_MANDEL_ILP",
+                    "OFL_REDUCE_CPS", "OFL_STENCIL_VARIANT", "OFL_STENCIL2D_VARIANT",
+                    "OFL_STREAM_VARIANT", "OFL_LIB", "OFL_NO_JIT")
+
+
+def refuse_variant_switches(args) -> None:
+    set_ = [k for k in VARIANT_SWITCHES if k in os.environ]
+    if set_ and not args.allow_variants:
+        raise SystemExit(f"bench.py: refusing to run with kernel-variant switches set: {set_} "
+                         "(unset them, or pass --allow-variants for a sweep)")
+
+
+def spawn_ranks(n: int, argv: list) -> None:
+    """--gpus N without torchrun: run N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1 and pass through rank 0's line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    # torchrun would read "--n" as an abbreviation of its own options
+    argv = ["--elements" if a == "--n" else
+            ("--elements=" + a[4:] if a.startswith("--n=") else a) for a in argv]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    r = subprocess.run(cmd)
+    if r.returncode:
+        raise SystemExit(r.returncode)
+
+
 def main(argv=None) -> None:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=1 << 25)
+    ap.add_argument("--elements", "--n", dest="n", type=int, default=1 << 25,
+                    help="triad elements per GPU (default 2^25, BASELINE config 1)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-sets", type=int, default=2,
                     help="device buffer sets / streams the e2e steps rotate over")
-    ap.add_argument("--overhead-steps", type=int, default=10000)
+    ap.add_argument("--overhead-ks", default="1,10,100,1000,10000,100000",
+                    help="chain lengths K of the per-future overhead sweep (config 5)")
     ap.add_argument("--no-overhead", action="store_true")
+    ap.add_argument("--allow-variants", action="store_true",
+                    help="permit OFL_* kernel-variant switches (sweeps only, never a headline)")
+    ap.add_argument("--configs", default="heat,mandelbrot,dot",
+                    help="BASELINE configs 2-4 measured after the headline (N=1 only); '' = none")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: approximate length of the K timed steps")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    refuse_variant_switches(args)
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # one process per GPU: launch ourselves under torchrun (same command
+        # line), exactly as the driver does for N>1
+        spawn_ranks(args.gpus, sys.argv[1:] if argv is None else list(argv))
+        return
+    if world is not None and int(world) != args.gpus and args.impl == "ours":
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU expected")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -17,8 +17,11 @@ validators bench/harness.py:123-158, tests/oracles.py:13-69):
 Pinning: both are checked against golden vectors produced by importing and
 running the reference itself (tests/golden/make_golden.py ->
 tests/golden/golden.json) and against the reference tests' known answers.
-The fp32 dot product has no reference implementation (the kernel language
-has no f32); its oracle is pinned only by its own fp64 restatement.
+The fp32 dot product has no reference kernel (the kernel language has no
+f32); it is pinned by the reference executor running the same arithmetic on
+f64 buffers holding the fp32 values (``dot_seq`` in make_golden.py, results
+in tests/golden/golden_long.json), which ``dot_f32_seq`` reproduces bit for
+bit and ``dot_f32`` (fixed 2^16 chunks) within 1e-12 relative.
 """
 
 from __future__ import annotations
@@ -63,6 +66,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_sum_u32.restype = u32
         L.oracle_dot_f32.argtypes = [vp, vp, u64, i32]
         L.oracle_dot_f32.restype = f64
+        L.oracle_dot_f32_seq.argtypes = [vp, vp, u64]
+        L.oracle_dot_f32_seq.restype = f64
         L.oracle_partition.argtypes = [vp, u32, u64, i32]
         L.oracle_partition.restype = None
         L.oracle_max_threads.argtypes = []
@@ -152,6 +157,14 @@ def dot_f32(a: np.ndarray, b: np.ndarray, threads: int = 1) -> float:
     a = np.ascontiguousarray(a, dtype=np.float32)
     b = np.ascontiguousarray(b, dtype=np.float32)
     return float(lib().oracle_dot_f32(_p(a), _p(b), min(a.size, b.size), threads))
+
+
+def dot_f32_seq(a: np.ndarray, b: np.ndarray) -> float:
+    """The reference executor's order (one work item, index order); pinned
+    bit for bit by tests/golden/golden_long.json."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    return float(lib().oracle_dot_f32_seq(_p(a), _p(b), min(a.size, b.size)))
 
 
 def partition(offset: int, count: int, threads: int = 1) -> np.ndarray:

@@ -308,6 +308,17 @@ double oracle_dot_f32(const float* a, const float* b, uint64_t n, int threads) {
   return total;
 }
 
+/* The reference's own order for the same dot product: the dot_seq kernel of
+ * tests/golden/make_golden.py (reference language, pattern
+ * bench/kernels/sum.k:3-11) run by the reference executor — work item 0
+ * adds the exact fp64 products of the fp32 values in index order.
+ * Bit-identical to golden_long.json["dot"]. */
+double oracle_dot_f32_seq(const float* a, const float* b, uint64_t n) {
+  double acc = 0.0;
+  for (uint64_t i = 0; i < n; ++i) acc = acc + (double)a[i] * (double)b[i];
+  return acc;
+}
+
 /* partition.k (bench/kernels/partition.k:3-8). */
 struct part_ctx {
   double* out;

@@ -329,20 +329,12 @@ def dot_cfg(rt, dev, out, n=1 << 31):
 
 
 def overhead_cfg(rt, dev, out):
-    from bench import overhead_sweep  # noqa: E402
+    from bench import OverheadBench  # noqa: E402
 
-    sweep = {}
-    for k in (1, 10, 100, 1000, 10000, 100000):
-        r = overhead_sweep(dev, rt, k, min(k, 2000))
-        sweep[str(k)] = r
-    sweep["4KiB_payload_10000"] = overhead_sweep(dev, rt, 10000, 1000, payload_bytes=4096)
-    sweep["note"] = (
-        "raw = the same cudaMemcpyAsync + STREAM launch from a C loop; c_abi = libofl "
-        "from Python without futures. With a 4 KiB payload the back-to-back C loop is "
-        "slower on the GPU side (12-13 us/step) than the same calls issued at the "
-        "C-ABI's pace (9-10 us/step), so its futurized overhead vs raw reads negative; "
-        "compare futurized against c_abi there (scripts/probes/overhead_payload.py)")
-    out["config5_overhead"] = sweep
+    out["config5_overhead"] = {
+        "8B_payload": OverheadBench(dev, rt).sweep(),
+        "4KiB_payload": OverheadBench(dev, rt, payload_bytes=4096).sweep((1, 100, 10000)),
+    }
 
 
 def stencil2d_cfg(rt, dev, out, w=16384, h=16384):

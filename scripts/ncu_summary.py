@@ -43,6 +43,31 @@ def raw(rep: str):
     return hdr, units, data
 
 
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+          "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def to_bytes(row, hdr, units, metric: str) -> float:
+    """One byte metric in bytes, with ITS OWN unit (ncu picks a unit per
+    metric: the read and write counters of one launch can differ)."""
+    i = hdr.index(metric)
+    u = units[i]
+    if u not in _SCALE:
+        raise ValueError(f"unknown unit {u!r} for {metric}")
+    return float(row[i].replace(",", "")) * _SCALE[u]
+
+
+def traffic(rep: str) -> list:
+    """[(kernel, read bytes, write bytes, duration ns)] per profiled launch."""
+    hdr, units, data = raw(rep)
+    ni, ti = hdr.index("Kernel Name"), hdr.index("gpu__time_duration.sum")
+    tscale = {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+              "second": 1e9, "s": 1e9}[units[ti]]
+    return [(r[ni], to_bytes(r, hdr, units, "dram__bytes_read.sum"),
+             to_bytes(r, hdr, units, "dram__bytes_write.sum"),
+             float(r[ti].replace(",", "")) * tscale) for r in data]
+
+
 def summarize(rep: str) -> str:
     hdr, units, data = raw(rep)
     lines = [f"ncu --set full capture: {rep}"]
@@ -54,11 +79,10 @@ def summarize(rep: str) -> str:
                 i = hdr.index(m)
                 lines.append(f"    {m} = {r[i]} {units[i]}")
         if "dram__bytes_read.sum" in hdr:
-            rd = float(r[hdr.index("dram__bytes_read.sum")])
-            wr = float(r[hdr.index("dram__bytes_write.sum")])
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            u = units[hdr.index("dram__bytes_read.sum")]
-            lines.append(f"    traffic (read+write) = {(rd + wr) * scale.get(u, 1):.0f} bytes")
+            rd = to_bytes(r, hdr, units, "dram__bytes_read.sum")
+            wr = to_bytes(r, hdr, units, "dram__bytes_write.sum")
+            lines.append(f"    dram read = {rd:.0f} bytes, dram write = {wr:.0f} bytes")
+            lines.append(f"    traffic (read+write) = {rd + wr:.0f} bytes")
     return "\n".join(lines)
 
 

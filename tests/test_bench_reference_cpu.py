@@ -35,3 +35,29 @@ def test_reference_arm_under_torchrun_env():
     assert r0.returncode == 0, r0.stderr[-2000:]
     line = json.loads(r0.stdout.strip().splitlines()[-1])
     assert line["config"]["parallelism"].startswith("2 independent")
+
+
+def test_gpus_flag_spawns_ranks_without_torchrun():
+    """`bench.py --gpus 2` outside torchrun launches 2 ranks itself (one per
+    GPU; here the CPU reference arm, where rank 0 alone reports)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--ref-seconds", "1", "--n", str(1 << 20)]
+    r = subprocess.run(cmd, cwd=REPO, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"].startswith("2 independent")
+
+
+def test_variant_switches_refused():
+    r = _run({"WORLD_SIZE": "1", "RANK": "0", "OFL_HEAT_TB": "8"})
+    assert r.returncode != 0 and "kernel-variant switches" in (r.stderr + r.stdout)
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--steps", "3", "--warmup", "3"],
+                       cwd=REPO, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr

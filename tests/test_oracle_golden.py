@@ -160,3 +160,35 @@ def test_dot_oracles_agree():
     assert abs(x - npo.dot_f32(a, b)) <= 1e-12 * abs(x)  # numpy sums pairwise
     exact = float(np.dot(a.astype(np.float64), b.astype(np.float64)))
     assert abs(x - exact) <= 1e-12 * abs(exact)
+
+
+# -- golden_long.json: the reference itself on config 2 / config 4 work ---------------
+
+def _long():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_long.json")) as fh:
+        return json.load(fh)
+
+
+def test_dot_seq_oracle_matches_reference_bit_for_bit():
+    """The reference executor's dot (dot_seq in make_golden.py: f64 buffers
+    holding fp32 values, index order) reproduced exactly by oracle.dot_f32_seq;
+    the chunked oracle the GPU tests use stays within 1e-12 of it."""
+    for case in _long()["dot"]:
+        rng = np.random.default_rng(case["seed"])
+        a = rng.random(case["n"], dtype=np.float32)
+        b = rng.random(case["n"], dtype=np.float32)
+        assert oracle.dot_f32_seq(a, b) == case["result"] == float.fromhex(case["result_hex"])
+        assert abs(oracle.dot_f32(a, b, threads=0) - case["result"]) <= 1e-12 * case["result"]
+
+
+def test_heat_1000_steps_oracle_matches_reference():
+    """2^20 cells x 1000 steps of the reference's stencil.k, ping-pong, run
+    by the reference executor (golden_long.json) == oracle.heat."""
+    for case in _long()["heat"]:
+        if case["n"] > 1 << 20:
+            continue  # 2^28 x 1000: GPU test only (tests/test_gpu_pinned.py)
+        x = np.random.default_rng(case["seed"]).random(case["n"])
+        assert sha(oracle.heat(x, case["steps"], threads=0)) == case["sha256"]
