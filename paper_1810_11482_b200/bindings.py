@@ -274,10 +274,12 @@ def _dot_launch(st, v, items, ticket):
 
 
 def heat_block() -> int:
-    """Most steps fused per HBM pass by the heat builtin (OFL_HEAT_TB, default
-    72 — the fastest measured cap, profiles/r01_heat_sweep.txt; the C side
-    spreads the steps evenly over the fewest passes of the right parity)."""
-    return max(1, min(128, int(os.environ.get("OFL_HEAT_TB", "72"))))
+    """Most steps fused per HBM pass by the heat builtin (default 96 — the
+    fastest measured cap for the production pass kernel, profiles/
+    r02_heat_sweep.txt; the C side spreads the steps evenly over the fewest
+    passes of the right parity).  OFL_HEAT_TB overrides it for the parity
+    tests of other schedules; bench.py refuses to run with it set."""
+    return max(1, min(128, int(os.environ.get("OFL_HEAT_TB", "96"))))
 
 
 def _heat_oob(v, items):

@@ -14,10 +14,10 @@
 // as one 128-bit vector; the outer neighbours come from the adjacent lanes by
 // warp shuffle, so every cell is read from HBM once: 16 B/cell.
 //
-// Temporal blocking (k_heat_tb): a CTA stages a tile of kTile cells plus a
-// halo of `tb` cells each side in shared memory, advances it `tb` steps in
-// place (the valid region shrinks by one cell per side per step), and writes
-// the centre back: 16 B/cell per `tb` steps instead of per step.  Global
+// Temporal blocking (k_heat_pipe, below): a warp holds a tile of cells plus
+// a halo of `tb` cells each side in registers, advances it `tb` steps (the
+// valid region shrinks by one cell per side per step), and writes the
+// centre back: 16 B/cell per `tb` steps instead of per step.  Global
 // endpoints are fixed points of the update, exactly as stencil.k.
 #include <cstdlib>
 
@@ -207,140 +207,23 @@ void launch_stencil(cudaStream_t cs, const double* x, double* y, uint64_t n, uin
 }
 
 // ---------------------------------------------------------------- heat ---
-constexpr int kTbThreads = 512;
-constexpr int kTile = 8192;  // cells written per CTA pass
-
-// One pass = `tb` steps over the whole vector (x -> y).  Tile t covers
-// cells [t*kTile, (t+1)*kTile); smem holds [t*kTile - tb, (t+1)*kTile + tb).
-__global__ void __launch_bounds__(kTbThreads) k_heat_tb(const double* __restrict__ x,
-                                                        double* __restrict__ y, uint64_t n,
-                                                        int tb) {
-  extern __shared__ double sm[];  // two buffers of kTile + 2*tb
-  const int w = kTile + 2 * tb;
-  double* a = sm;
-  double* b = sm + w;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t g0 = (int64_t)(t * kTile) - tb;  // global index of smem[0]
-    for (int k = threadIdx.x; k < w; k += kTbThreads) {
-      const int64_t g = g0 + k;
-      a[k] = (g >= 0 && g < (int64_t)n) ? __ldcs(x + g) : 0.0;
-    }
-    __syncthreads();
-    for (int s = 1; s <= tb; ++s) {
-      // valid after s steps: smem [s, w - s)
-      for (int k = s + threadIdx.x; k < w - s; k += kTbThreads) {
-        const int64_t g = g0 + k;
-        double v;
-        if (g <= 0 || g >= (int64_t)n - 1) v = a[k];
-        else v = point(a[k - 1], a[k], a[k + 1]);
-        b[k] = v;
-      }
-      __syncthreads();
-      double* tmp = a;
-      a = b;
-      b = tmp;
-    }
-    for (int k = tb + threadIdx.x; k < tb + kTile; k += kTbThreads) {
-      const int64_t g = g0 + k;
-      if (g < (int64_t)n) __stcs(y + g, a[k]);
-    }
-    __syncthreads();
-  }
-}
-
-// Register-blocked temporal blocking.  A CTA of kRegThreads threads holds a
-// tile of kRegThreads*R consecutive cells in registers (thread t owns cells
-// [t*R, t*R+R) of the tile), advances it `tb` steps without touching memory
-// — in-warp neighbours by shuffle, warp-edge cells through a double-
-// buffered shared array, one __syncthreads per step — and writes the centre
-// kRegThreads*R - 2*tb cells.  Errors from the clamped tile ends travel one
-// cell per step, so they stay inside the tb-cell halo.  Shared-memory
-// traffic per cell-step drops from ~32 B (k_heat_tb) to ~2 warp-edge words,
-// which leaves the FP64 pipe (4 DP ops per cell-step) as the limiter.
-constexpr int kRegThreads = 256;
-
-// One step of the register tile: in[] -> out[] (distinct register arrays,
-// so an unrolled pair of steps needs no register moves).  Step parity p
-// selects the half of the warp-edge exchange buffer.
-template <int R>
-__device__ __forceinline__ void reg_step(const double (&in)[R], double (&out)[R],
-                                         double (*edge_l)[kRegThreads / 32],
-                                         double (*edge_r)[kRegThreads / 32], int p, int lane,
-                                         int warp, bool edge, int64_t g0, int64_t nn) {
-  constexpr int kWarps = kRegThreads / 32;
-  if (lane == 0) edge_l[p][warp] = in[0];
-  if (lane == 31) edge_r[p][warp] = in[R - 1];
-  double left = __shfl_up_sync(0xffffffffu, in[R - 1], 1);
-  double right = __shfl_down_sync(0xffffffffu, in[0], 1);
-  __syncthreads();
-  if (lane == 0) left = warp > 0 ? edge_r[p][warp - 1] : in[0];
-  if (lane == 31) right = warp < kWarps - 1 ? edge_l[p][warp + 1] : in[R - 1];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const double l = i > 0 ? in[i - 1] : left;
-    const double r = i + 1 < R ? in[i + 1] : right;
-    out[i] = point(l, in[i], r);
-  }
-  if (edge) {  // rare: my cells include global cell 0 or n-1 (held fixed)
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int64_t g = g0 + i;
-      if (g <= 0 || g >= nn - 1) out[i] = in[i];
-    }
-  }
-}
-
-template <int R>
-__global__ void __launch_bounds__(kRegThreads) k_heat_reg(const double* __restrict__ x,
-                                                          double* __restrict__ y, uint64_t n,
-                                                          int tb) {
-  constexpr int kWarps = kRegThreads / 32;
-  constexpr int kCells = kRegThreads * R;
-  __shared__ double edge_l[2][kWarps];  // first cell of each warp
-  __shared__ double edge_r[2][kWarps];  // last cell of each warp
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t valid = kCells - 2 * tb;
-  const int64_t t0 = (int64_t)blockIdx.x * valid - tb;  // global index of tile cell 0
-  const int64_t g0 = t0 + (int64_t)threadIdx.x * R;      // global index of my c[0]
-  const int64_t nn = (int64_t)n;
-
-  double a[R], b[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t g = g0 + i;
-    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
-  }
-  // does my range contain a global endpoint (0 or n-1)?  rare
-  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
-
-  int s = 0;
-  for (; s + 1 < tb; s += 2) {
-    reg_step<R>(a, b, edge_l, edge_r, 0, lane, warp, edge, g0, nn);
-    reg_step<R>(b, a, edge_l, edge_r, 1, lane, warp, edge, g0, nn);
-  }
-  const bool odd = s < tb;
-  if (odd) reg_step<R>(a, b, edge_l, edge_r, 0, lane, warp, edge, g0, nn);
-  // write the valid centre [tb, kCells - tb) of the tile
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int local = threadIdx.x * R + i;
-    const int64_t g = g0 + i;
-    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) y[g] = odd ? b[i] : a[i];
-  }
-}
-
-// Warp-independent variant: every warp owns its own tile of 32*R cells
-// (halo tb each side, computed redundantly), so a step needs two shuffles
-// and no barrier at all; per-thread ILP (R independent cells) hides latency
-// instead of occupancy.
+// T steps of stencil.k (BASELINE config 2) in passes of up to tb steps; a
+// pass keeps each tile in registers for all its steps, so HBM sees 16 B per
+// cell per pass instead of per step and the FP64 pipe is the bound.  Earlier
+// forms (shared-memory tiles, CTA register tiles with a barrier per step,
+// two-level warp ghosts, one tile per warp; profiles/r01_heat_sweep.txt,
+// r02_heat_sweep.txt) were removed once this one beat them.
+// Warp tiles: every warp owns its own tile of 32*R consecutive cells (R per
+// lane, in registers) including a halo of tb cells each side that is
+// computed redundantly, so a step needs two shuffles and no barrier at all;
+// per-thread ILP (R independent cells) hides the FP64 latency.
 constexpr int kWarpThreads = 128;
 
 // Fused form of point(): when 0.5*l and 0.5*r are exact (no result below
 // 2^-1022), round(0.5*l + c) is exactly __dadd_rn(__dmul_rn(0.5, l), c), so
 //   (0.5*l + c) + 0.5*r  ==  fma(0.5, r, fma(0.5, l, c))      bit for bit
 // — two DFMA instead of DMUL + 2 DADD (3 after CSE).  Only valid under the
-// tile guard in k_heat_warp (heat_fma_safe).
+// tile guard (warp_tile_steps).
 __device__ __forceinline__ double point_fma(double l, double c, double r) {
   return __fma_rn(0.5, r, __fma_rn(0.5, l, c));
 }
@@ -426,37 +309,30 @@ struct SlabOut {
   double* right;  // receives y[own_hi - h, own_hi), or null
 };
 
-// Residency by tile size (profiles/r01_heat_sweep.txt): four 128-thread
-// CTAs per SM for R <= 24 (128 registers), three for R <= 30 (168), two
-// above.  Default R=30 at 3 CTAs/SM: 41.2 ms for config 2 (R=24 at 4 CTAs:
-// 43.9; 13% instead of 17% redundant halo cells outweighs the lower
-// residency); R=32 at 3 CTAs spills inside the step loop (50.0 ms).
-// The slab form (extra peer stores) would spill at 128, so it gets three.
 template <int R, bool kSlab>
-constexpr int heat_warp_min_blocks() {
-  return kSlab ? 3 : (R <= 24 ? 4 : (R <= 30 ? 3 : 2));
-}
-
-template <int R, bool kSlab = false>
-__global__ void __launch_bounds__(kWarpThreads, heat_warp_min_blocks<R, kSlab>()) k_heat_warp(const double* __restrict__ x,
-                                                            double* __restrict__ y, uint64_t n,
-                                                            int tb, bool fma_ok,
-                                                            SlabOut so = SlabOut{}) {
+__device__ __noinline__ void heat_tile_slow(const double* __restrict__ x, double* __restrict__ y,
+                                            int64_t nn, int tb, bool fma_ok, int64_t g0, int lane,
+                                            int64_t own_lo, int64_t own_hi, int64_t h,
+                                            double* left, double* right) {
   constexpr int kCells = 32 * R;
-  const int lane = threadIdx.x & 31;
-  const int64_t wtile = (int64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
-  const int64_t valid = kCells - 2 * tb;
-  const int64_t nn = (int64_t)n;
-  const int64_t g0 = wtile * valid - tb + (int64_t)lane * R;
-  if (wtile * valid >= nn) return;  // whole warp past the end (warp-uniform)
   double a[R], b[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int64_t g = g0 + i;
     a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
   }
-  const bool edge = (g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1);
-  const bool odd = warp_tile_steps<R>(a, b, lane, edge, g0, nn, tb, fma_ok);
+  bool fused = fma_ok;
+  if (fused) {
+    const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020), see warp_tile_steps
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
+      fused &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
+    }
+  }
+  fused = __all_sync(0xffffffffu, fused);
+  const bool odd = fused ? warp_steps<R, true, true>(a, b, lane, g0, nn, tb)
+                         : warp_steps<R, false, true>(a, b, lane, g0, nn, tb);
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int local = lane * R + i;
@@ -465,134 +341,220 @@ __global__ void __launch_bounds__(kWarpThreads, heat_warp_min_blocks<R, kSlab>()
       const double v = odd ? b[i] : a[i];
       if (!kSlab) {
         y[g] = v;
-      } else if (g >= so.own_lo && g < so.own_hi) {
+      } else if (g >= own_lo && g < own_hi) {
         y[g] = v;
-        if (so.left && g < so.own_lo + so.h) so.left[g - so.own_lo] = v;
-        if (so.right && g >= so.own_hi - so.h) so.right[g - (so.own_hi - so.h)] = v;
+        if (left && g < own_lo + h) left[g - own_lo] = v;
+        if (right && g >= own_hi - h) right[g - (own_hi - h)] = v;
       }
     }
   }
 }
 
-// Two-level temporal blocking.  Each warp runs warp-independent steps (two
-// shuffles, no barrier) on a warp tile of 32*R cells whose outer K cells on
-// each side are ghosts (K <= R/2, so they live in lanes 0 and 31); every K
-// steps the warps refresh their ghosts from their neighbours' boundary cells
-// through double-buffered shared memory (one barrier per K steps).  The
-// CTA's outer tb cells are the tile halo.  Redundant work drops from 2*tb per
-// warp (k_heat_warp) to 2*K per warp + 2*tb per CTA, barriers from one per
-// step (k_heat_reg) to one per K steps.
-constexpr int kHierWarps = 4;
-
-// lanes 0 / 31 publish their first / last K owned cells, barrier, then pull
-// the neighbours' into their ghosts (static register indices only)
-template <int R, int K>
-__device__ __forceinline__ void ghost_exchange(double (&c)[R], double (*sl)[K], double (*sr)[K],
-                                               int lane, int warp) {
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) sl[warp][i] = c[K + i];
-  }
-  if (lane == 31) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) sr[warp][i] = c[R - 2 * K + i];
-  }
-  __syncthreads();
-  if (lane == 0 && warp > 0) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) c[i] = sr[warp - 1][i];
-  }
-  if (lane == 31 && warp < kHierWarps - 1) {
-#pragma unroll
-    for (int i = 0; i < K; ++i) c[R - K + i] = sl[warp + 1][i];
-  }
+// Persistent warps with the tiles moved by the bulk-copy engine (TMA).
+// Every warp owns one shared-memory tile buffer (32R+2 doubles) and an
+// mbarrier, and walks its tiles t = warp, warp + W, ...:
+//   * the NEXT tile's cells are prefetched into the buffer by one
+//     cp.async.bulk while the current tile is advanced in registers, so the
+//     HBM load overlaps the FP64 work instead of every warp of an SM loading
+//     at the same moment (one-tile-per-warp grids run in lock step: all
+//     warps load, then all compute, and the FP64 pipe idles ~16% of a pass);
+//   * at the end of a tile each lane swaps its R results with its R cells of
+//     the prefetched tile (registers <-> shared memory), and the valid centre
+//     goes back to HBM with one cp.async.bulk store, read out of the buffer
+//     before the following prefetch overwrites it;
+//   * global loads and stores are whole contiguous tiles (the register
+//     layout, R consecutive cells per lane, would make them 32-way strided).
+// Tiles touching global cell 0 or n-1, or reaching past n, and tiles that
+// fail the fused-update guard run heat_tile_slow (global loads/stores).
+// Alignment: a tile's load starts at the even index lo & ~1 and spans 32R+2
+// cells; the valid centre starts at the even index t*valid (valid = 32R-2tb)
+// and sits at the even buffer offset tb + (tb & 1): both 16-byte aligned.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
 }
 
-// tb steps of the two-level scheme: K barrier-free warp steps, then a ghost
-// refresh from the neighbouring warps; returns whether the state is in a.
-template <int R, int K, bool kFma, bool kEdge>
-__device__ __forceinline__ bool hier_steps(double (&a)[R], double (&b)[R], int lane, int warp,
-                                           int64_t g0, int64_t nn, int tb,
-                                           double (*sh_l)[kHierWarps][K],
-                                           double (*sh_r)[kHierWarps][K]) {
-  int s = 0, ex = 0;
-  bool in_a = true;
-  while (s < tb) {
-    int k = 0;
-    for (; k + 1 < K && s + k + 1 < tb; k += 2) {
-      if (in_a) {
-        warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
-        warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
-      } else {
-        warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
-        warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
-      }
-    }
-    if (k < K && s + k < tb) {
-      if (in_a) warp_step<R, kFma, kEdge>(a, b, lane, g0, nn);
-      else warp_step<R, kFma, kEdge>(b, a, lane, g0, nn);
-      in_a = !in_a;
-      ++k;
-    }
-    s += k;
-    if (s >= tb) break;
-    const int p = ex & 1;
-    ++ex;
-    if (in_a)
-      ghost_exchange<R, K>(a, sh_l[p], sh_r[p], lane, warp);
-    else
-      ghost_exchange<R, K>(b, sh_l[p], sh_r[p], lane, warp);
-  }
-  return in_a;
+__device__ __forceinline__ void bulk_load(uint32_t dst, const double* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
 }
 
-template <int R, int K>
-__global__ void __launch_bounds__(kHierWarps * 32) k_heat_hier(const double* __restrict__ x,
-                                                               double* __restrict__ y,
-                                                               uint64_t n, int tb, bool fma_ok) {
-  static_assert(2 * K <= R, "ghosts must fit in the edge lanes");
-  constexpr int kOwn = 32 * R - 2 * K;        // owned cells per warp
-  constexpr int kSpan = kHierWarps * kOwn;    // owned cells per CTA (incl. CTA halo)
-  __shared__ double sh_l[2][kHierWarps][K];   // each warp's first K owned cells
-  __shared__ double sh_r[2][kHierWarps][K];   // each warp's last K owned cells
+template <int R>
+__host__ __device__ constexpr int heat_pipe_buf() {  // doubles per warp buffer (16-byte multiple)
+  return 32 * R + 2;
+}
+
+// cells per lane of the production heat pass (odd: conflict-free 8-byte
+// shared-memory accesses at a lane stride of R doubles)
+constexpr int kHeatPipeR = 99;
+
+template <int R>
+constexpr int heat_pipe_min_blocks() {
+  return R <= 63 ? 3 : 2;
+}
+
+// Tiles are handed out by an atomic counter (grabbed one tile ahead, so
+// the prefetch can start): the few tiles the pipeline cannot take — those
+// holding global cell 0 or n-1 or reaching past n-1 — come first and run
+// the general path before the pipelined loop, so no call sits inside the
+// loop (its live values would be spilled) and the warps that took them
+// simply grab fewer tiles later.  The counter is reset once per heat call;
+// pass p of a call reads it relative to `base` (every pass hands out
+// exactly ntiles + warps values: each warp stops at its first index past
+// the end).
+template <int R, bool kSlab = false>
+__global__ void __launch_bounds__(kWarpThreads, heat_pipe_min_blocks<R>())
+    k_heat_pipe(const double* __restrict__ x, double* __restrict__ y, uint64_t n, int tb,
+                bool fma_ok, unsigned long long* ctr, unsigned long long base,
+                SlabOut so = SlabOut{}) {
+  constexpr int kCells = 32 * R;
+  constexpr int kBuf = heat_pipe_buf<R>();
+  constexpr int kWarps = kWarpThreads / 32;
+  extern __shared__ __align__(128) double heat_smem[];
+  __shared__ __align__(8) uint64_t bars[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* buf = heat_smem + warp * kBuf;
+  const uint32_t buf_a = static_cast<uint32_t>(__cvta_generic_to_shared(buf));
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&bars[warp]));
   const int64_t nn = (int64_t)n;
-  const int64_t cta0 = (int64_t)blockIdx.x * (kSpan - 2 * tb) - tb;  // global of CTA owned[0]
-  const int64_t g0 = cta0 + (int64_t)warp * kOwn - K + (int64_t)lane * R;  // my c[0]
+  const int64_t valid = kCells - 2 * tb;
+  const int64_t ntiles = (nn + valid - 1) / valid;
+  // eligible tiles are [t_lo, t_hi]: lo = t*valid - tb >= 1, the aligned
+  // load range [lo & ~1, (lo & ~1) + kBuf) ends at or before n-1, and (slab
+  // passes) the stored centre lies inside the owned cells minus the strips
+  // that go to the neighbours' ghost cells
+  const int64_t own_lo = kSlab ? so.own_lo + (so.left ? so.h : 0) : 0;
+  const int64_t own_hi = kSlab ? so.own_hi - (so.right ? so.h : 0) : nn;
+  int64_t t_lo = (tb + 1 + valid - 1) / valid;
+  if (kSlab && t_lo * valid < own_lo) t_lo = (own_lo + valid - 1) / valid;
+  int64_t t_hi = (nn - 1 - kBuf + tb + 1) / valid;  // (lo & ~1) <= lo <= lo+1
+  if (t_hi > ntiles - 1) t_hi = ntiles - 1;
+  while (t_hi >= 0 && (((t_hi * valid - tb) & ~(int64_t)1) + kBuf > nn - 1 ||
+                       (kSlab && t_hi * valid + valid > own_hi)))
+    --t_hi;
+  const int64_t n_elig = t_hi >= t_lo ? t_hi - t_lo + 1 : 0;
+  const int64_t n_edge = ntiles - n_elig;  // handed out first
+  // hand-out order: tiles [0, t_lo), then (t_hi, ntiles), then [t_lo, t_hi]
+  auto tile_of = [&](int64_t k) -> int64_t {
+    if (n_elig == 0) return k;
+    if (k < n_edge) return k < t_lo ? k : t_hi + 1 + (k - t_lo);
+    return t_lo + (k - n_edge);
+  };
+  auto grab = [&]() -> int64_t {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1ull) - base;
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  // valid is even, so every tile's first cell t*valid - tb has the parity
+  // of tb: one buffer offset d for all tiles
+  const int d = tb & 1;
+  auto prefetch = [&](int64_t tile) {  // lane 0 only
+    const int64_t lo_al = (tile * valid - tb) & ~(int64_t)1;
+    bulk_load(buf_a, x + lo_al, kBuf * 8u, bar);
+  };
+  int64_t k = grab();
+  while (k < n_edge) {  // edge / overhanging tiles: general path, global memory
+    const int64_t te = tile_of(k);
+    heat_tile_slow<R, kSlab>(x, y, nn, tb, fma_ok, te * valid - tb + (int64_t)lane * R, lane,
+                             so.own_lo, so.own_hi, so.h, so.left, so.right);
+    k = grab();
+  }
+  if (k >= ntiles) return;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
   double a[R], b[R];
+  int64_t t = tile_of(k);
+  if (lane == 0) prefetch(t);
+  mbar_wait(bar, phase);
+  phase ^= 1;
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t g = g0 + i;
-    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
-  }
-  // CTA-uniform update form: ghosts carry neighbouring warps' values into a
-  // warp's tile, so the fused update's guard (warp_tile_steps) must hold for
-  // the whole CTA tile; the endpoint fix-up is likewise decided per CTA
-  bool safe = fma_ok;
-  if (safe) {
-    const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020)
+  for (int i = 0; i < R; ++i) a[i] = buf[lane * R + d + i];
+  bool store_pending = false;  // lane 0's bulk store may still be reading the buffer
+  while (true) {
+    const int64_t kn = grab();
+    const bool next = kn < ntiles;
+    const int64_t tn = next ? tile_of(kn) : 0;
+    // the buffer is free once every lane has read the current tile out of
+    // it and the previous bulk store has read its results
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0 && store_pending) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+    if (next && lane == 0) prefetch(tn);
+    bool fused = fma_ok;
+    if (fused) {
+      const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020), see warp_tile_steps
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
-      safe &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
+      for (int i = 0; i < R; ++i) {
+        const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
+        fused &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
+      }
     }
-  }
-  safe = __syncthreads_and(safe);
-  const bool edge = __syncthreads_or((g0 <= 0 && g0 + R > 0) || (g0 <= nn - 1 && g0 + R > nn - 1));
-  bool in_a;
-  if (safe)
-    in_a = edge ? hier_steps<R, K, true, true>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r)
-                : hier_steps<R, K, true, false>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r);
-  else
-    in_a = edge ? hier_steps<R, K, false, true>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r)
-                : hier_steps<R, K, false, false>(a, b, lane, warp, g0, nn, tb, sh_l, sh_r);
+    fused = __all_sync(0xffffffffu, fused);
+    const int64_t g0 = t * valid - tb + (int64_t)lane * R;
+    if (fused) {
+      int s = 0;
+      for (; s + 1 < tb; s += 2) {
+        warp_step<R, true, false>(a, b, lane, g0, nn);
+        warp_step<R, true, false>(b, a, lane, g0, nn);
+      }
+      if (s < tb) {
+        warp_step<R, true, false>(a, b, lane, g0, nn);
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int own = warp * kOwn - K + lane * R + i;  // CTA owned coordinate
-    const int64_t g = g0 + i;
-    const bool mine = (lane * R + i >= K) && (lane * R + i < 32 * R - K);
-    if (mine && own >= tb && own < kSpan - tb && g >= 0 && g < nn) y[g] = in_a ? a[i] : b[i];
+        for (int i = 0; i < R; ++i) a[i] = b[i];
+      }
+    } else {  // rare (signs, -0, tiny values): the unfused update, same tile
+      int s = 0;
+      for (; s + 1 < tb; s += 2) {
+        warp_step<R, false, false>(a, b, lane, g0, nn);
+        warp_step<R, false, false>(b, a, lane, g0, nn);
+      }
+      if (s < tb) {
+        warp_step<R, false, false>(a, b, lane, g0, nn);
+#pragma unroll
+        for (int i = 0; i < R; ++i) a[i] = b[i];
+      }
+    }
+    if (next) {
+      mbar_wait(bar, phase);  // the next tile has landed
+      phase ^= 1;
+      // results of t into the buffer, cells of tn into registers
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double v = buf[lane * R + d + i];
+        buf[lane * R + d + i] = a[i];
+        a[i] = v;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < R; ++i) buf[lane * R + d + i] = a[i];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(y + t * valid),
+                   "r"(buf_a + (uint32_t)(tb + d) * 8u), "r"((uint32_t)valid * 8u)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    store_pending = true;
+    if (!next) break;
+    t = tn;
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 }  // namespace
@@ -614,45 +576,15 @@ extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n
   return q.finish(ticket);
 }
 
-// heat pass kernel (OFL_HEAT_KERNEL): 2 = warp-independent register tiles
-// (default, fastest measured), 0 = CTA register tiles with a barrier per
-// step, 1 = shared-memory tiles, 3 = two-level (warp ghosts + CTA halo)
-static int heat_kernel() {
-  static int v = [] {
-    const char* e = getenv("OFL_HEAT_KERNEL");
-    return e ? atoi(e) : 2;
-  }();
-  return v;
-}
-
-// cells per thread of the register kernels (OFL_HEAT_R: 8, 16, 20, 24, 26, 28, 30, 32);
-// default per kernel from profiles/r01_heat_sweep.txt
-static int heat_cells_per_thread() {
-  static int v = [] {
-    const char* e = getenv("OFL_HEAT_R");
-    const int dflt = heat_kernel() == 2 ? 30 : 8;
-    const int r = e ? atoi(e) : dflt;
-    return (r == 8 || r == 16 || r == 20 || r == 24 || r == 26 || r == 28 || r == 30 || r == 32) ? r : dflt;
-  }();
-  return v;
-}
-
-// fused two-DFMA update under the tile guard (OFL_HEAT_FMA=0 disables; the
-// unfused kernel is kept for the sweep and for tiles the guard rejects)
-static bool heat_fused() {
-  static bool v = [] {
-    const char* e = getenv("OFL_HEAT_FMA");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return v;
-}
+// Fused two-DFMA update under the tile guard (always on; the unfused update
+// runs for tiles the guard rejects).
+static bool heat_fused() { return true; }
 
 extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_t steps, int tb,
                         uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (n < 1) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat needs n >= 1");
   if (tb < 1 || tb > 128) return ofl::set_error(OFL_ERR_BAD_ARGS, "temporal block must be 1..128");
-  if (heat_kernel() != 2 && tb > 64) tb = 64;  // the sweep kernels size their tiles for <= 64
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat operands must be 16-byte aligned");
   ofl::Enqueue q(s);
@@ -660,9 +592,6 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
   const int sms = ofl::num_sms(s->dev);
   double* src = x;
   double* dst = y;
-  const size_t smem = sizeof(double) * 2 * (kTile + 2 * 64);
-  // per-device attribute; cheap to (re)apply
-  cudaFuncSetAttribute(k_heat_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // Pass schedule: the fewest passes of at most tb steps whose count has the
   // parity of `steps` (each pass swaps the buffers, so the state must end
   // where the single-step ping-pong would leave it: x if steps is even, else
@@ -671,66 +600,39 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
   uint64_t passes = (steps + (uint64_t)tb - 1) / (uint64_t)tb;
   if ((passes & 1) != (steps & 1)) ++passes;
   const uint64_t base_k = passes ? steps / passes : 0, longer = passes ? steps % passes : 0;
+  constexpr int R = kHeatPipeR;
+  const int smem = (int)(sizeof(double) * (kWarpThreads / 32) * heat_pipe_buf<R>());
+  const uint64_t cap = (uint64_t)sms * heat_pipe_min_blocks<R>();
+  unsigned long long* ctr = nullptr;  // k_heat_pipe's tile counter, reset once per call
+  unsigned long long base = 0;        // values the earlier passes of this call handed out
   uint64_t launches = 0;
-  auto run_pass = [&](int k) -> cudaError_t {
+  for (uint64_t i = 0; i < passes; ++i) {
+    const int k = (int)(base_k + (i < longer ? 1 : 0));
     if (k == 1) {
       launch_stencil(s->cs, src, dst, n, n);
-    } else if (heat_kernel() == 1) {
-      const uint64_t ntiles = (n + kTile - 1) / kTile;
-      uint64_t blocks = ntiles < (uint64_t)sms * 2 ? ntiles : (uint64_t)sms * 2;
-      const size_t sm_k = sizeof(double) * 2 * (kTile + 2 * k);
-      k_heat_tb<<<(unsigned)blocks, kTbThreads, sm_k, s->cs>>>(src, dst, n, k);
-    } else if (heat_kernel() == 3) {
-      const int r = heat_cells_per_thread();
-      constexpr int K = 8;
-      const uint64_t span = (uint64_t)kHierWarps * (32 * (uint64_t)r - 2 * K);
-      const uint64_t valid = span - 2 * (uint64_t)k;
-      const unsigned blocks = (unsigned)((n + valid - 1) / valid);
-      if (r == 24)
-        k_heat_hier<24, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k, heat_fused());
-      else
-        k_heat_hier<16, K><<<blocks, kHierWarps * 32, 0, s->cs>>>(src, dst, n, k, heat_fused());
-    } else if (heat_kernel() == 2) {
-      const int r = heat_cells_per_thread();
-      const bool fma = heat_fused();
-      const uint64_t valid = 32ull * r - 2 * (uint64_t)k;
-      const uint64_t warps = (n + valid - 1) / valid;
-      const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
-      if (r == 32)
-        k_heat_warp<32><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else if (r == 24)
-        k_heat_warp<24><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else if (r == 20)
-        k_heat_warp<20><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else if (r == 28)
-        k_heat_warp<28><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else if (r == 26)
-        k_heat_warp<26><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else if (r == 30)
-        k_heat_warp<30><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
-      else
-        k_heat_warp<16><<<blocks, kWarpThreads, 0, s->cs>>>(src, dst, n, k, fma);
     } else {
-      const int r = heat_cells_per_thread();
-      const uint64_t valid = (uint64_t)kRegThreads * r - 2 * (uint64_t)k;
-      const unsigned blocks = (unsigned)((n + valid - 1) / valid);
-      if (r == 8)
-        k_heat_reg<8><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
-      else if (r == 32)
-        k_heat_reg<32><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
-      else
-        k_heat_reg<16><<<blocks, kRegThreads, 0, s->cs>>>(src, dst, n, k);
+      if (!ctr) {
+        void* scratch = nullptr;
+        const int st = ofl::stream_scratch(s, 65536, &scratch);
+        if (st) return st;
+        ctr = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + 40960);
+        cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s->cs);
+        if (e != cudaSuccess) return ofl::cuda_error(e, "heat counter reset");
+        cudaFuncSetAttribute(k_heat_pipe<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      }
+      const uint64_t valid = 32ull * R - 2 * (uint64_t)k;
+      const uint64_t tiles = (n + valid - 1) / valid;
+      const uint64_t want = (tiles + kWarpThreads / 32 - 1) / (kWarpThreads / 32);
+      const unsigned blocks = (unsigned)(want < cap ? want : cap);
+      k_heat_pipe<R><<<blocks, kWarpThreads, smem, s->cs>>>(src, dst, n, k, heat_fused(), ctr, base);
+      base += tiles + (uint64_t)blocks * (kWarpThreads / 32);
     }
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return ofl::cuda_error(e, "heat launch");
     ++launches;
     double* t = src;
     src = dst;
     dst = t;
-    return cudaPeekAtLastError();
-  };
-  for (uint64_t i = 0; i < passes; ++i) {
-    const int k = (int)(base_k + (i < longer ? 1 : 0));
-    cudaError_t e = run_pass(k);
-    if (e != cudaSuccess) return ofl::cuda_error(e, "heat launch");
   }
   ofl::count_launch(launches);
   return q.finish(ticket);
@@ -745,17 +647,35 @@ extern "C" int ofl_heat_slab(ofl_stream* s, const double* x, double* y, uint64_t
   if (own_lo > own_hi || own_hi > n || h > own_hi - own_lo)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: bad owned range / halo");
   if (x == y) return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab: x and y must differ");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab operands must be 16-byte aligned");
   if (left_ghost && left_dev != s->dev) ofl::enable_peer(s->dev, left_dev);
   if (right_ghost && right_dev != s->dev) ofl::enable_peer(s->dev, right_dev);
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
   SlabOut so{(int64_t)own_lo, (int64_t)own_hi, (int64_t)h, h ? left_ghost : nullptr,
              h ? right_ghost : nullptr};
-  const uint64_t valid = 32ull * 24 - 2 * (uint64_t)k;
-  const uint64_t warps = (n + valid - 1) / valid;
-  const unsigned blocks = (unsigned)((warps + kWarpThreads / 32 - 1) / (kWarpThreads / 32));
-  k_heat_warp<24, true><<<blocks, kWarpThreads, 0, s->cs>>>(x, y, n, k, heat_fused(), so);
-  cudaError_t e = cudaPeekAtLastError();
+  // the single-device pass kernel (k_heat_pipe) with the slab epilogue: tiles
+  // whose centre reaches the strips sent to the neighbours run the general
+  // path, which also stores those strips into the peers' ghost cells
+  constexpr int R = kHeatPipeR;
+  const int sms = ofl::num_sms(s->dev);
+  const uint64_t valid = 32ull * R - 2 * (uint64_t)k;
+  const uint64_t tiles = (n + valid - 1) / valid;
+  const uint64_t want = (tiles + kWarpThreads / 32 - 1) / (kWarpThreads / 32);
+  const uint64_t cap = (uint64_t)sms * heat_pipe_min_blocks<R>();
+  const unsigned blocks = (unsigned)(want < cap ? want : cap);
+  void* scratch = nullptr;
+  const int st = ofl::stream_scratch(s, 65536, &scratch);
+  if (st) return st;
+  auto* ctr = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) + 40960);
+  cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s->cs);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "heat slab counter reset");
+  const int smem = (int)(sizeof(double) * (kWarpThreads / 32) * heat_pipe_buf<R>());
+  cudaFuncSetAttribute(k_heat_pipe<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_heat_pipe<R, true><<<blocks, kWarpThreads, smem, s->cs>>>(x, y, n, k, heat_fused(), ctr, 0ull,
+                                                               so);
+  e = cudaPeekAtLastError();
   if (e != cudaSuccess) return ofl::cuda_error(e, "heat slab launch");
   ofl::count_launch();
   return q.finish(ticket);
