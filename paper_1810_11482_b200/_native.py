@@ -179,7 +179,8 @@ def _bind_fast(lib) -> None:
         _fast = None
         return
     addr = lambda fn: ctypes.cast(fn, ctypes.c_void_p).value  # noqa: E731
-    _oflcall.bind(addr(lib.ofl_h2d), addr(lib.ofl_stream_op), addr(lib.ofl_wait))
+    _oflcall.bind(addr(lib.ofl_h2d), addr(lib.ofl_stream_op), addr(lib.ofl_wait),
+                  addr(lib.ofl_query))
     _fast = _oflcall
 
 

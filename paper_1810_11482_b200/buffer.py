@@ -97,6 +97,22 @@ class BufferObject:
                 raise_status(status, "write")
         return DeviceToken(st, ticket.value)
 
+    def write_pinned(self, offset: int, data, stream: int = 0) -> CompletionToken:
+        """enqueue_write of a ``pinned_empty`` array (zero-copy DMA): the
+        handles' fast path, range already checked by the handle."""
+        fast = _native._fast
+        if fast is None or not data.flags.c_contiguous:
+            return self.enqueue_write(offset, data, stream)
+        n = data.nbytes
+        dev = self.device
+        st = dev._streams.get(stream) or dev.stream(stream)
+        t = fast.h2d(st.ptr, self.ptr + offset, data._address(), n)
+        if t < 0:
+            raise_status(-t, "write")
+        if n:
+            st.keep(t, data)
+        return DeviceToken(st, t)
+
     def enqueue_read(self, offset: int, size: int, stream: int = 0) -> CompletionToken:
         """Token for the bytes of [offset, offset+size) at this stream position."""
         check_range(offset, size, self.size_bytes, "read")

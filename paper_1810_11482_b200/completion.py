@@ -160,7 +160,15 @@ class DeviceToken(CompletionToken):
         if self._state != _PENDING:
             return True
         s = self._stream
-        if s.done_ticket() < self._ticket:
+        fast = _native._fast
+        if fast is not None:  # ofl_query checks the done watermark first
+            r = fast.query(s.ptr, self._ticket)
+            if r < 0:
+                self._fail(-r, "device operation failed")
+                return True
+            if not r:
+                return False
+        elif s.done_ticket() < self._ticket:
             ready = ctypes.c_int(0)
             status = s.lib.ofl_query(s.ptr, self._ticket, ctypes.byref(ready))
             if status:

@@ -8,7 +8,8 @@
  * ctypes library (`bind`), so the one library the rest of the runtime uses —
  * including a substitute loaded through OFL_LIB — is the one called.
  *
- * Every call releases the GIL around the C call (as ctypes does) and returns
+ * Every call that can block releases the GIL around the C call (as ctypes
+ * does; query never blocks: a cudaEventQuery) and returns
  * the operation's ticket, or -status when libofl reports an error (wait
  * returns the status), so the caller raises exactly what the ctypes path
  * raises (_native.error_for).
@@ -22,10 +23,12 @@ typedef int (*stream_op_fn)(void*, int, double*, const double*, const double*, d
                             uint64_t*);
 
 typedef int (*wait_fn)(void*, uint64_t);
+typedef int (*query_fn)(void*, uint64_t, int*);
 
 static copy_fn p_h2d = NULL;
 static stream_op_fn p_stream_op = NULL;
 static wait_fn p_wait = NULL;
+static query_fn p_query = NULL;
 
 static int as_u64(PyObject* o, uint64_t* out) {
   if (o == Py_None) {
@@ -43,23 +46,44 @@ static PyObject* result(int status, uint64_t ticket) {
   return PyLong_FromUnsignedLongLong(ticket);
 }
 
-/* bind(addr_ofl_h2d, addr_ofl_stream_op, addr_ofl_wait) */
+/* bind(addr_ofl_h2d, addr_ofl_stream_op, addr_ofl_wait[, addr_ofl_query]) */
 static PyObject* oc_bind(PyObject* self, PyObject* const* args, Py_ssize_t n) {
   (void)self;
-  uint64_t a, b, c;
-  if (n != 3) {
-    PyErr_SetString(PyExc_TypeError, "bind expects 3 function addresses");
+  uint64_t a, b, c, d = 0;
+  if (n != 3 && n != 4) {
+    PyErr_SetString(PyExc_TypeError, "bind expects 3 or 4 function addresses");
     return NULL;
   }
-  if (as_u64(args[0], &a) || as_u64(args[1], &b) || as_u64(args[2], &c)) return NULL;
-  if (!a || !b || !c) {
+  if (as_u64(args[0], &a) || as_u64(args[1], &b) || as_u64(args[2], &c) ||
+      (n == 4 && as_u64(args[3], &d)))
+    return NULL;
+  if (!a || !b || !c || (n == 4 && !d)) {
     PyErr_SetString(PyExc_ValueError, "null function address");
     return NULL;
   }
   p_h2d = (copy_fn)(uintptr_t)a;
   p_stream_op = (stream_op_fn)(uintptr_t)b;
   p_wait = (wait_fn)(uintptr_t)c;
+  p_query = (query_fn)(uintptr_t)d;
   Py_RETURN_NONE;
+}
+
+/* query(stream, ticket) -> 1 ready | 0 pending | -status   (ofl_query; never blocks) */
+static PyObject* oc_query(PyObject* self, PyObject* const* args, Py_ssize_t n) {
+  (void)self;
+  uint64_t s, ticket;
+  if (n != 2) {
+    PyErr_SetString(PyExc_TypeError, "query expects 2 arguments");
+    return NULL;
+  }
+  if (!p_query) {
+    PyErr_SetString(PyExc_RuntimeError, "_oflcall query not bound");
+    return NULL;
+  }
+  if (as_u64(args[0], &s) || as_u64(args[1], &ticket)) return NULL;
+  int ready = 0;
+  const int status = p_query((void*)(uintptr_t)s, ticket, &ready);
+  return PyLong_FromLong(status ? -(long)status : (ready ? 1 : 0));
 }
 
 /* wait(stream, ticket) -> status   (ofl_wait; blocks with the GIL released) */
@@ -137,6 +161,8 @@ static PyMethodDef methods[] = {
     {"bind", (PyCFunction)(void (*)(void))oc_bind, METH_FASTCALL, "bind libofl entry points"},
     {"h2d", (PyCFunction)(void (*)(void))oc_h2d, METH_FASTCALL, "ofl_h2d -> ticket | -status"},
     {"wait", (PyCFunction)(void (*)(void))oc_wait, METH_FASTCALL, "ofl_wait -> status"},
+    {"query", (PyCFunction)(void (*)(void))oc_query, METH_FASTCALL,
+     "ofl_query -> 1 ready | 0 pending | -status"},
     {"stream_op", (PyCFunction)(void (*)(void))oc_stream_op, METH_FASTCALL,
      "ofl_stream_op -> ticket | -status"},
     {NULL, NULL, 0, NULL},

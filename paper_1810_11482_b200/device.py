@@ -93,12 +93,18 @@ class Stream:
 
     def wait_ticket(self, ticket: int) -> int:
         """Block until `ticket` completed; returns the C status."""
+        fast = _native._fast
+        if fast is not None:
+            return fast.wait(self.ptr, ticket)
         return self.lib.ofl_wait(self.ptr, ticket)
 
     def error(self, status: int) -> Exception:
         return _native.error_for(status, f"{self.device.info.name} stream {self.sid}")
 
     def query_ticket(self, ticket: int) -> bool:
+        fast = _native._fast
+        if fast is not None:
+            return fast.query(self.ptr, ticket) > 0
         ready = ctypes.c_int(0)
         status = self.lib.ofl_query(self.ptr, ticket, ctypes.byref(ready))
         return bool(ready.value) and not status
