@@ -120,6 +120,17 @@ int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint64_t bytes,
                      uint64_t* ticket);
 /* host-to-host copy on the library's copy threads (staging <-> pageable) */
 int ofl_host_memcpy(void* dst, const void* src, uint64_t bytes);
+/* D2H into a pinned staging block in `chunk`-byte pieces, each followed by
+ * an event; *out receives the pending read (one ticket for the whole read).
+ * ofl_collect waits for each piece and copies it to the pageable `dst` on
+ * the copy threads while later pieces are still in flight — the staging
+ * half of BufferObject.enqueue_read returning `bytes` (buffer.py:49-55).
+ * ofl_read_release frees the handle (after ofl_collect, or unobserved). */
+typedef struct ofl_read ofl_read;
+int ofl_d2h_chunked(ofl_stream* s, void* staging, const void* src, uint64_t bytes,
+                    uint64_t chunk, ofl_read** out, uint64_t* ticket);
+int ofl_collect(ofl_read* r, void* dst);
+int ofl_read_release(ofl_read* r);
 /* cross-device copy over NVLink (peer access enabled on first use) */
 int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev,
             uint64_t bytes, uint64_t* ticket);

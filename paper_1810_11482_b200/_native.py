@@ -71,6 +71,10 @@ _SIGNATURES = {
     "ofl_d2d": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_h2d_pageable": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),
     "ofl_host_memcpy": (c_int, [c_void_p, c_void_p, c_uint64]),
+    "ofl_d2h_chunked": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, c_uint64,
+                                ctypes.POINTER(c_void_p), _u64p]),
+    "ofl_collect": (c_int, [c_void_p, c_void_p]),
+    "ofl_read_release": (c_int, [c_void_p]),
     "ofl_p2p": (c_int, [_c_stream, c_void_p, c_int, c_void_p, c_int, c_uint64, _u64p]),
     "ofl_stream_wait": (c_int, [_c_stream, _c_stream, c_uint64]),
     "ofl_query": (c_int, [_c_stream, c_uint64, POINTER(c_int)]),
@@ -180,7 +184,7 @@ def _bind_fast(lib) -> None:
         return
     addr = lambda fn: ctypes.cast(fn, ctypes.c_void_p).value  # noqa: E731
     _oflcall.bind(addr(lib.ofl_h2d), addr(lib.ofl_stream_op), addr(lib.ofl_wait),
-                  addr(lib.ofl_query))
+                  addr(lib.ofl_query), addr(lib.ofl_collect))
     _fast = _oflcall
 
 

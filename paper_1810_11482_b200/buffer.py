@@ -119,6 +119,8 @@ class BufferObject:
         if size == 0:
             return make_ready(b"")
         st = self.device.stream(stream)
+        if size >= hostmem.CHUNKED_READ:
+            return self._read_chunked(st, offset, size, None)
         block = hostmem.pool.get(size)
         ticket = ctypes.c_uint64()
         status = st.lib.ofl_d2h(st.ptr, block.addr, self.ptr + offset, size, ctypes.byref(ticket))
@@ -148,6 +150,8 @@ class BufferObject:
                 raise_status(status, "read")
             st.keep(ticket.value, owner)
             return DeviceToken(st, ticket.value, lambda: out)
+        if n >= hostmem.CHUNKED_READ:
+            return self._read_chunked(st, offset, n, (addr, owner, out))
         block = hostmem.pool.get(n)
         status = st.lib.ofl_d2h(st.ptr, block.addr, self.ptr + offset, n, ctypes.byref(ticket))
         if status:
@@ -157,6 +161,24 @@ class BufferObject:
         st.keep(ticket.value, landing.release_later)
         return DeviceToken(st, ticket.value, lambda: (landing.take(), out)[1])
 
+
+    def _read_chunked(self, st, offset: int, n: int, into) -> CompletionToken:
+        """Large read to pageable memory: chunked D2H into a pinned staging
+        block (one event per chunk); the token's finish step copies each
+        chunk out on the copy threads as soon as it lands (ofl_collect), into
+        a new ``bytes`` (into=None) or into the caller's buffer."""
+        block = hostmem.pool.get(n)
+        handle = ctypes.c_void_p()
+        ticket = ctypes.c_uint64()
+        status = st.lib.ofl_d2h_chunked(st.ptr, block.addr, self.ptr + offset, n,
+                                        hostmem.READ_CHUNK, ctypes.byref(handle),
+                                        ctypes.byref(ticket))
+        if status:
+            hostmem.pool.put(block)
+            raise_status(status, "read")
+        landing = _ChunkedLanding(st.lib, block, n, handle.value, into)
+        st.keep(ticket.value, landing.release_later)
+        return DeviceToken(st, ticket.value, landing.take)
 
     def enqueue_read_rows_into(self, offset: int, out, row_bytes: int, rows: int,
                                dst_offset: int, dst_pitch: int, stream: int = 0):
@@ -235,6 +257,72 @@ class _Landing:
         if self.block is not None and self.purged:
             try:
                 hostmem.pool.put(self.block)
+            except Exception:  # noqa: BLE001
+                pass
+
+
+class _ChunkedLanding:
+    """A chunked read in flight (ofl_d2h_chunked): `take` collects it (waits
+    for each chunk, copies it out in parallel) and recycles the staging
+    block; dropped unobserved, the handle and block are released once the
+    stream has passed the read."""
+
+    __slots__ = ("lib", "block", "size", "handle", "into", "lock", "taken", "purged")
+
+    def __init__(self, lib, block, size: int, handle: int, into):
+        self.lib, self.block, self.size, self.handle, self.into = lib, block, size, handle, into
+        self.lock = threading.Lock()
+        self.taken = False
+        self.purged = False
+
+    def take(self):
+        with self.lock:
+            if self.taken:
+                raise RuntimeError("read collected twice")
+            self.taken = True
+            try:
+                if self.into is None:
+                    fast = _native._fast
+                    if fast is not None:
+                        out = fast.collect_bytes(self.handle, self.size)
+                        if type(out) is int:
+                            raise_status(-out, "read")
+                        return out
+                    out = bytearray(self.size)
+                    raw = (ctypes.c_char * self.size).from_buffer(out)
+                    status = self.lib.ofl_collect(self.handle, ctypes.addressof(raw))
+                    del raw
+                    if status:
+                        raise_status(status, "read")
+                    return bytes(out)
+                addr, _owner, result = self.into
+                status = self.lib.ofl_collect(self.handle, addr)
+                if status:
+                    raise_status(status, "read")
+                return result
+            finally:
+                self._release()
+
+    def release_later(self):
+        with self.lock:
+            self.purged = True
+            if not self.taken:
+                return  # the token's finish step will collect it
+            self._release()
+
+    def _release(self):
+        if self.handle:
+            self.lib.ofl_read_release(self.handle)
+            self.handle = 0
+        if self.block is not None:
+            hostmem.pool.put(self.block)
+            self.block = None
+
+    def __del__(self):
+        # token dropped unobserved after the copy completed
+        if self.handle and self.purged:
+            try:
+                self._release()
             except Exception:  # noqa: BLE001
                 pass
 

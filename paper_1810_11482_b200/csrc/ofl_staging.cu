@@ -1,16 +1,26 @@
-// Pageable host -> device writes (BufferObject.enqueue_write with a plain
-// `bytes`/numpy payload; reference buffer.py:40-47 makes three host copies).
+// Host side of large transfers between pageable memory and HBM.
 //
-// The payload is cut into chunks that are copied into a ring of pinned
-// staging slots by a small pool of host threads and DMA'd from there, so the
-// host copy of chunk k+1 overlaps the PCIe transfer of chunk k.  The caller
+// Writes (BufferObject.enqueue_write with a plain `bytes`/numpy payload; the
+// reference makes three host copies, buffer.py:40-47): the payload is cut
+// into chunks that the copy threads stage into a ring of pinned slots; each
+// chunk is DMA'd as soon as its copy is done, while the copies of the next
+// chunks proceed, so host copies and the PCIe transfer overlap.  The caller
 // returns once the last chunk is staged: the payload may then be reused, as
 // in the reference (which owns a copy once the call returns).  The stream
-// lock is held for the whole write, so the write stays one atomic stream
-// operation with one ticket.
+// lock is held for the whole write, so it stays one atomic stream operation
+// with one ticket.
+//
+// Reads (BufferObject.enqueue_read -> `bytes`, buffer.py:49-55): the D2H
+// goes to a pinned staging block in chunks, each followed by an event
+// (ofl_d2h_chunked); collecting (ofl_collect, run by the token's finish
+// step) waits for each chunk's event and hands it to the copy threads, so
+// the copy into the pageable destination of chunk k overlaps the DMA of the
+// chunks after it.
+#include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
-#include <functional>
+#include <deque>
 #include <thread>
 #include <vector>
 
@@ -18,83 +28,95 @@
 
 namespace {
 
-constexpr size_t kSlotBytes = 8u << 20;  // 8 MiB per slot
-constexpr int kSlots = 8;                // 64 MiB of pinned staging per process
-constexpr int kCopyThreads = 4;
+constexpr size_t kSlotBytes = 8u << 20;  // 8 MiB per staging slot
+constexpr int kSlots = 8;                // 64 MiB of pinned write staging per process
+constexpr size_t kPart = 1u << 20;       // copy task granularity
+constexpr int kLag = 3;                  // chunks being copied ahead of the DMA issue
 
-struct Slot {
-  void* host = nullptr;
-  cudaEvent_t done = nullptr;  // recorded after the slot's DMA
-  int dev = -1;
-  bool used = false;
+// A fixed pool of copy threads taking independent memcpy tasks; a Group
+// counts the outstanding tasks of one chunk (or of one whole copy).
+struct Group {
+  std::atomic<int> left{0};
+  std::mutex mu;
+  std::condition_variable cv;
+  void done_one() {
+    if (left.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+      std::lock_guard<std::mutex> g(mu);
+      cv.notify_all();
+    }
+  }
+  void wait() {
+    if (left.load(std::memory_order_acquire) == 0) return;
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return left.load(std::memory_order_acquire) == 0; });
+  }
 };
 
-struct Ring {
-  std::mutex mu;  // one staged write at a time
-  Slot slots[kSlots];
-  int next = 0;
+struct Task {
+  char* dst;
+  const char* src;
+  size_t n;
+  Group* g;
 };
-Ring g_ring;
 
-// minimal fork-join pool for the host copies
 class CopyPool {
  public:
   CopyPool() {
-    for (int i = 0; i < kCopyThreads; ++i) workers_.emplace_back([this] { loop(); });
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int n = (int)std::max(2u, std::min(12u, hw ? hw - 1 : 4u));
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
-  ~CopyPool() {
+  // split [src, src+n) -> dst into kPart tasks counted by g
+  void submit(void* dst, const void* src, size_t n, Group* g) {
+    const size_t parts = (n + kPart - 1) / kPart;
+    g->left.fetch_add((int)parts, std::memory_order_acq_rel);
     {
-      std::lock_guard<std::mutex> g(mu_);
-      stop_ = true;
+      std::lock_guard<std::mutex> lk(mu_);
+      for (size_t off = 0; off < n; off += kPart)
+        q_.push_back(Task{(char*)dst + off, (const char*)src + off, std::min(kPart, n - off), g});
     }
     cv_.notify_all();
-    for (auto& t : workers_) t.join();
   }
-  // copy [src, src+n) to dst using all workers plus the caller
+  // copy now, using the pool and the calling thread
   void copy(void* dst, const void* src, size_t n) {
-    const size_t parts = kCopyThreads + 1;
-    const size_t per = (n + parts - 1) / parts;
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      pending_ = 0;
-      for (size_t p = 1; p < parts; ++p) {
-        const size_t lo = p * per;
-        if (lo >= n) break;
-        const size_t len = (lo + per <= n) ? per : n - lo;
-        jobs_.push_back([=] { std::memcpy((char*)dst + lo, (const char*)src + lo, len); });
-        ++pending_;
+    Group g;
+    submit(dst, src, n, &g);
+    help(&g);
+    g.wait();
+  }
+  // run queued tasks on the calling thread until g is done or the queue is empty
+  void help(Group* g) {
+    while (g->left.load(std::memory_order_acquire) > 0) {
+      Task t;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (q_.empty()) return;
+        t = q_.front();
+        q_.pop_front();
       }
+      std::memcpy(t.dst, t.src, t.n);
+      t.g->done_one();
     }
-    cv_.notify_all();
-    std::memcpy(dst, src, per < n ? per : n);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [this] { return pending_ == 0; });
   }
 
  private:
   void loop() {
     for (;;) {
-      std::function<void()> job;
+      Task t;
       {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [this] { return stop_ || !jobs_.empty(); });
-        if (stop_) return;
-        job = std::move(jobs_.back());
-        jobs_.pop_back();
+        cv_.wait(lk, [this] { return !q_.empty(); });
+        t = q_.front();
+        q_.pop_front();
       }
-      job();
-      {
-        std::lock_guard<std::mutex> g(mu_);
-        if (--pending_ == 0) done_cv_.notify_all();
-      }
+      std::memcpy(t.dst, t.src, t.n);
+      t.g->done_one();
     }
   }
   std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  std::vector<std::function<void()>> jobs_;
+  std::condition_variable cv_;
+  std::deque<Task> q_;
   std::vector<std::thread> workers_;
-  int pending_ = 0;
-  bool stop_ = false;
 };
 
 CopyPool& pool() {
@@ -102,18 +124,56 @@ CopyPool& pool() {
   return *p;
 }
 
+struct Slot {
+  void* host = nullptr;
+  cudaEvent_t done = nullptr;  // recorded after the slot's DMA
+  int dev = -1;
+  bool used = false;
+  Group copied;                // the slot's host copy
+};
+
+struct Ring {
+  std::mutex mu;  // one staged write at a time
+  Slot slots[kSlots];
+};
+Ring g_ring;
+
+int prepare_slot(Slot& slot, int dev) {
+  cudaError_t e;
+  if (!slot.host) {
+    e = cudaHostAlloc(&slot.host, kSlotBytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) return ofl::cuda_error(e, "staging cudaHostAlloc");
+  }
+  if (slot.used) {
+    e = cudaEventSynchronize(slot.done);  // the slot's previous DMA finished
+    if (e != cudaSuccess) return ofl::cuda_error(e, "staging slot wait");
+    slot.used = false;
+  }
+  if (slot.dev != dev) {  // events belong to a device
+    if (slot.done) cudaEventDestroy(slot.done);
+    e = cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return ofl::cuda_error(e, "staging event");
+    slot.dev = dev;
+  }
+  return OFL_OK;
+}
+
 }  // namespace
 
-// Host memcpy on the copy pool (large staging <-> pageable copies).
+// pending chunked device->host read (ofl_d2h_chunked / ofl_collect)
+struct ofl_read {
+  int dev;
+  const char* staging;
+  uint64_t bytes, chunk;
+  std::vector<cudaEvent_t> events;  // one per chunk, recorded after its DMA
+};
+
+// Host memcpy on the copy threads (large staging <-> pageable copies).
 extern "C" int ofl_host_memcpy(void* dst, const void* src, uint64_t bytes) {
-  if (bytes >= (4u << 20)) {
-    static std::mutex mu;  // the pool runs one fork-join copy at a time
-    std::lock_guard<std::mutex> g(mu);
-    std::lock_guard<std::mutex> r(g_ring.mu);
+  if (bytes >= (4u << 20))
     pool().copy(dst, src, (size_t)bytes);
-  } else if (bytes) {
+  else if (bytes)
     std::memcpy(dst, src, (size_t)bytes);
-  }
   return OFL_OK;
 }
 
@@ -123,35 +183,101 @@ extern "C" int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint6
   std::lock_guard<std::mutex> ring_lock(g_ring.mu);
   ofl::Enqueue q(s);
   if (!q.ok()) return q.status;
-  uint64_t off = 0;
-  while (off < bytes) {
-    Slot& slot = g_ring.slots[g_ring.next];
-    g_ring.next = (g_ring.next + 1) % kSlots;
-    cudaError_t e;
-    if (!slot.host) {
-      e = cudaHostAlloc(&slot.host, kSlotBytes, cudaHostAllocPortable);
-      if (e != cudaSuccess) return ofl::cuda_error(e, "staging cudaHostAlloc");
-    }
-    if (slot.used) {
-      e = cudaEventSynchronize(slot.done);  // the slot's previous DMA finished
-      if (e != cudaSuccess) return ofl::cuda_error(e, "staging slot wait");
-    }
-    if (slot.dev != s->dev) {  // events belong to a device
-      if (slot.done) cudaEventDestroy(slot.done);
-      e = cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming);
-      if (e != cudaSuccess) return ofl::cuda_error(e, "staging event");
-      slot.dev = s->dev;
-    }
-    const size_t len = bytes - off < kSlotBytes ? (size_t)(bytes - off) : kSlotBytes;
-    if (len >= (1u << 20))
-      pool().copy(slot.host, (const char*)src + off, len);
-    else
-      std::memcpy(slot.host, (const char*)src + off, len);
-    e = cudaMemcpyAsync((char*)dst + off, slot.host, len, cudaMemcpyHostToDevice, s->cs);
+  const uint64_t nchunks = (bytes + kSlotBytes - 1) / kSlotBytes;
+  auto len_of = [&](uint64_t k) {
+    return (size_t)std::min<uint64_t>(kSlotBytes, bytes - k * kSlotBytes);
+  };
+  // chunk k uses slot k % kSlots; its copy is submitted kLag chunks before
+  // its DMA is issued, so up to kLag chunks are being staged while the
+  // caller waits for the oldest one and hands it to the copy engine
+  auto stage = [&](uint64_t k) -> int {
+    Slot& slot = g_ring.slots[k % kSlots];
+    const int st = prepare_slot(slot, s->dev);
+    if (st) return st;
+    pool().submit(slot.host, (const char*)src + k * kSlotBytes, len_of(k), &slot.copied);
+    return OFL_OK;
+  };
+  int status = OFL_OK;
+  uint64_t staged = 0;
+  for (uint64_t k = 0; k < nchunks && status == OFL_OK; ++k) {
+    while (staged < nchunks && staged <= k + kLag && status == OFL_OK) status = stage(staged++);
+    if (status) break;
+    Slot& slot = g_ring.slots[k % kSlots];
+    pool().help(&slot.copied);
+    slot.copied.wait();
+    cudaError_t e = cudaMemcpyAsync((char*)dst + k * kSlotBytes, slot.host, len_of(k),
+                                    cudaMemcpyHostToDevice, s->cs);
     if (e == cudaSuccess) e = cudaEventRecord(slot.done, s->cs);
-    if (e != cudaSuccess) return ofl::cuda_error(e, "staged H2D");
+    if (e != cudaSuccess) status = ofl::cuda_error(e, "staged H2D");
     slot.used = true;
-    off += len;
   }
+  // never leave copy tasks running into slots after an error
+  for (auto& slot : g_ring.slots) slot.copied.wait();
+  if (status) return status;
   return q.finish(ticket);
+}
+
+extern "C" int ofl_d2h_chunked(ofl_stream* s, void* staging, const void* src, uint64_t bytes,
+                               uint64_t chunk, ofl_read** out, uint64_t* ticket) {
+  OFL_CHECK_STREAM(s);
+  if (!out || !staging || !chunk) return ofl::set_error(OFL_ERR_BAD_ARGS, "d2h_chunked arguments");
+  *out = nullptr;
+  auto* r = new ofl_read{s->dev, (const char*)staging, bytes, chunk, {}};
+  ofl::Enqueue q(s);
+  if (!q.ok()) {
+    delete r;
+    return q.status;
+  }
+  for (uint64_t off = 0; off < bytes; off += chunk) {
+    const uint64_t len = std::min(chunk, bytes - off);
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync((char*)staging + off, (const char*)src + off, len,
+                          cudaMemcpyDeviceToHost, s->cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, s->cs);
+    if (e != cudaSuccess) {
+      for (auto x : r->events) cudaEventDestroy(x);
+      delete r;
+      return ofl::cuda_error(e, "chunked D2H");
+    }
+    r->events.push_back(ev);
+  }
+  const int st = q.finish(ticket);
+  if (st) {
+    for (auto x : r->events) cudaEventDestroy(x);
+    delete r;
+    return st;
+  }
+  *out = r;
+  return OFL_OK;
+}
+
+extern "C" int ofl_collect(ofl_read* r, void* dst) {
+  if (!r) return ofl::set_error(OFL_ERR_BAD_ARGS, "null read handle");
+  cudaError_t e = ofl::use_device(r->dev);
+  if (e != cudaSuccess) return ofl::cuda_error(e, "cudaSetDevice");
+  Group g;
+  int status = OFL_OK;
+  for (size_t i = 0; i < r->events.size(); ++i) {
+    e = cudaEventSynchronize(r->events[i]);
+    if (e != cudaSuccess) {
+      status = ofl::cuda_error(e, "device fault");
+      break;
+    }
+    const uint64_t off = i * r->chunk;
+    pool().submit((char*)dst + off, r->staging + off, (size_t)std::min(r->chunk, r->bytes - off),
+                  &g);
+  }
+  pool().help(&g);
+  g.wait();
+  return status;
+}
+
+extern "C" int ofl_read_release(ofl_read* r) {
+  if (!r) return OFL_OK;
+  if (ofl::use_device(r->dev) == cudaSuccess)
+    for (auto x : r->events) cudaEventDestroy(x);
+  delete r;
+  return OFL_OK;
 }

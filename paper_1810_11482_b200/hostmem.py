@@ -27,6 +27,8 @@ import numpy as np
 from . import _native
 
 SMALL_PAGEABLE = 256 * 1024  # below this, let the driver stage pageable data
+CHUNKED_READ = 4 << 20       # reads to pageable memory from this size: chunked, collected in parallel
+READ_CHUNK = 8 << 20         # D2H piece of a chunked read
 _MIN_CLASS = 4096
 
 _ranges_lock = threading.Lock()

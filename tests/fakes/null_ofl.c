@@ -81,3 +81,8 @@ int ofl_gate_signal(void* s, void* c, uint64_t v, uint64_t* t) { (void)c; (void)
 int ofl_gate_wait(void* s, const void* c, int n, uint64_t tg, void* st, uint64_t* t) { (void)c; (void)n; (void)tg; (void)st; return op(s, t); }
 int ofl_h2d_pageable(void* s, void* d, const void* x, uint64_t n, uint64_t* t) { memcpy(d, x, n); return op(s, t); }
 int ofl_host_memcpy(void* d, const void* s, uint64_t n) { memcpy(d, s, n); return 0; }
+typedef struct { void* staging; uint64_t bytes; } R;
+int ofl_d2h_chunked(void* s, void* st, const void* x, uint64_t n, uint64_t c, void** out, uint64_t* t) {
+  (void)c; memcpy(st, x, n); R* r = malloc(sizeof(R)); r->staging = st; r->bytes = n; *out = r; return op(s, t); }
+int ofl_collect(void* r, void* dst) { memcpy(dst, ((R*)r)->staging, ((R*)r)->bytes); return 0; }
+int ofl_read_release(void* r) { free(r); return 0; }

@@ -136,6 +136,20 @@ SCRIPT = textwrap.dedent(
         while not got and time.time() - t0 < 5:
             time.sleep(0.01)
         assert got == ["OobAccessError"], got
+        # large reads to pageable memory: chunked D2H collected in parallel
+        huge = d0.create_buffer((9 << 20) + 24).get()
+        pl = np.random.default_rng(2).integers(0, 256, (9 << 20) + 24, dtype=np.uint8)
+        huge.enqueue_write(0, pl)                     # pageable staged write (> 8 MiB: 2 slots)
+        assert huge.enqueue_read(0, pl.size).get() == pl.tobytes()
+        assert huge.enqueue_read(8, 5 << 20).get() == pl[8:8 + (5 << 20)].tobytes()
+        o = bytearray(pl.size)
+        assert huge.enqueue_read_into(0, o).get() is o and bytes(o) == pl.tobytes()
+        o2 = np.zeros(6 << 20, np.uint8)
+        assert when_all([huge.enqueue_read_into(16, o2)]).get() is None
+        assert o2.tobytes() == pl[16:16 + (6 << 20)].tobytes()
+        dropped = huge.enqueue_read(0, pl.size)
+        del dropped
+        d0.synchronize().get()
         bad3 = DeviceToken(st, tk, boom)
         assert when_all([when_all([bad3])]).is_failed()
 
