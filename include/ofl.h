@@ -82,8 +82,15 @@ void* ofl_stream_handle(ofl_stream* s);
 /* ---- memory: replaces DeviceObject.allocate/release + BufferObject storage
  *      (device.py:217-228, buffer.py:26-38); device memory is zero-filled
  *      like np.zeros (buffer.py:32) ----------------------------------------- */
+/* ofl_malloc: from the device's stream-ordered pool (cudaMallocAsync);
+ * ofl_free of such a buffer is ordered on the device after the work enqueued
+ * so far on every stream of the process (cudaFreeAsync after fence events),
+ * never a device-wide synchronisation.  ofl_malloc_shareable: a plain
+ * cudaMalloc allocation that ofl_ipc_handle can export (stream-ordered
+ * allocations have no CUDA IPC handle); ofl_free releases it with cudaFree. */
 int ofl_malloc(int dev, uint64_t bytes, void** dptr);
-/* CUDA IPC: share a device allocation (from ofl_malloc) with the other
+int ofl_malloc_shareable(int dev, uint64_t bytes, void** dptr);
+/* CUDA IPC: share a device allocation (from ofl_malloc_shareable) with the other
  * processes of the node (one process per GPU); handles are 64 bytes.  Used
  * by the fused cross-process reduction (collectives.ProcessPeerGroup). */
 int ofl_ipc_handle(void* dptr, char* out64);

@@ -57,6 +57,7 @@ _SIGNATURES = {
     "ofl_stream_done": (c_uint64, [_c_stream]),
     "ofl_stream_handle": (c_void_p, [_c_stream]),
     "ofl_malloc": (c_int, [c_int, c_uint64, POINTER(c_void_p)]),
+    "ofl_malloc_shareable": (c_int, [c_int, c_uint64, POINTER(c_void_p)]),
     "ofl_free": (c_int, [c_int, c_void_p]),
     "ofl_host_alloc": (c_int, [c_uint64, POINTER(c_void_p)]),
     "ofl_host_free": (c_int, [c_void_p]),

@@ -618,9 +618,9 @@ class ProcessHeatSlabs:
         self.bounds = decomp.shard_bounds(x.size, self.world)
         sl = self.layout[self.rank]
         local = np.ascontiguousarray(np.asarray(x, dtype=np.float64)[sl.start : sl.start + sl.length])
-        self.bufs = [device.create_buffer(local.nbytes).get() for _ in range(2)]
+        self.bufs = [device.create_buffer(local.nbytes, shareable=True).get() for _ in range(2)]
         self.bufs[0].enqueue_write(0, local.tobytes())
-        self.block = device.create_buffer(64).get()  # [0] counter, [8] status
+        self.block = device.create_buffer(64, shareable=True).get()  # [0] counter, [8] status
         objs = [rt.local._buffer(b.gid) for b in (*self.bufs, self.block)]
         self.ordinal = objs[0].device.ordinal
         self.stream = objs[0].device.stream(0)

@@ -37,13 +37,13 @@ class BufferObject:
 
     __slots__ = ("device", "size_bytes", "ptr", "__weakref__")
 
-    def __init__(self, device: DeviceObject, size_bytes: int):
+    def __init__(self, device: DeviceObject, size_bytes: int, shareable: bool = False):
         if size_bytes <= 0:
             raise BadArgsError("buffer size must be positive")
         self.device = device
         self.size_bytes = size_bytes
         self.ptr = 0
-        self.ptr = device.allocate(size_bytes)
+        self.ptr = device.allocate(size_bytes, shareable)
 
     def __del__(self):
         if self.ptr:

@@ -173,7 +173,7 @@ class ProcessPeerGroup:
         self.world = dist.get_world_size(group)
         if not 1 <= self.world <= 16:
             raise BadArgsError("a peer group has 1..16 members")
-        self.block = device.create_buffer(lib.ofl_xchg_bytes()).get()
+        self.block = device.create_buffer(lib.ofl_xchg_bytes(), shareable=True).get()
         obj = rt.local._buffer(self.block.gid)
         self.ordinal = obj.device.ordinal
         handle = ctypes.create_string_buffer(64)

@@ -36,6 +36,9 @@ struct ofl_stream {
   // per-stream device scratch for multi-block reductions / work queues
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // recorded by ofl_free to order a stream-ordered free after this stream's
+  // work enqueued so far (the free's stream waits on it)
+  cudaEvent_t fence = nullptr;
 };
 
 struct ofl_event {

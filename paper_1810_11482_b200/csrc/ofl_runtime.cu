@@ -15,6 +15,9 @@
 #include <memory>
 #include <vector>
 
+#include <set>
+#include <unordered_set>
+
 #include "ofl_internal.h"
 
 namespace ofl {
@@ -173,9 +176,51 @@ static void CUDART_CB host_complete(void* p) {
   delete pl;
 }
 
-// ----------------------------------------------------------- zero fill ---
+// ------------------------------------------------------------- memory ---
+// Buffers come from each device's stream-ordered memory pool (cudaMallocAsync
+// on a per-device internal stream; the pool keeps freed memory for reuse
+// instead of returning it to the driver).  A free is ordered on the device
+// after the work enqueued so far on every stream of the process — the
+// internal stream waits on a fence event recorded on each, then
+// cudaFreeAsync — instead of cudaFree's implicit device-wide
+// synchronisation, which stalled every stream (including other devices'
+// fused exchanges) whenever a buffer was dropped.  Buffers shared with other
+// processes through CUDA IPC are plain cudaMalloc allocations (IPC handles
+// do not cover stream-ordered allocations): ofl_malloc_shareable.
 static std::mutex g_zero_mu[kMaxDev];
-static cudaStream_t g_zero_stream[kMaxDev];
+static cudaStream_t g_zero_stream[kMaxDev];  // allocation + zero fill
+static std::mutex g_free_mu[kMaxDev];
+static cudaStream_t g_free_stream[kMaxDev];  // frees, each after fence waits
+static bool g_pool_ready[kMaxDev];
+static std::mutex g_streams_mu;                 // live streams (free fences)
+static std::set<ofl_stream*> g_streams;
+static std::mutex g_legacy_mu;                  // cudaMalloc'd (shareable) buffers
+static std::unordered_set<void*> g_legacy;
+
+// the internal stream of `dev` (created on first use; caller holds g_zero_mu[dev])
+static cudaError_t internal_stream(int dev) {
+  if (g_zero_stream[dev]) return cudaSuccess;
+  return cudaStreamCreateWithFlags(&g_zero_stream[dev], cudaStreamNonBlocking);
+}
+
+static cudaError_t pool_setup(int dev) {
+  if (g_pool_ready[dev]) return cudaSuccess;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = UINT64_MAX;  // never trim at synchronisation points
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e != cudaSuccess) return e;
+  // an allocation may reuse memory whose free has already completed, but
+  // the pool must not make the allocation stream wait on a pending free
+  // (that would turn every allocation after a free into a wait for the
+  // work the free is ordered after)
+  int no = 0;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+  if (e != cudaSuccess) return e;
+  g_pool_ready[dev] = true;
+  return cudaSuccess;
+}
 
 // Direct peer access for copies and kernel peer stores (once per pair).
 static std::mutex g_peer_mu;
@@ -193,6 +238,15 @@ void enable_peer(int from, int to) {
     cudaSetDevice(from);
     cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
     if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+    // stream-ordered allocations need an explicit grant per accessing device
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, to) == cudaSuccess) {
+      cudaMemAccessDesc d{};
+      d.location.type = cudaMemLocationTypeDevice;
+      d.location.id = from;
+      d.flags = cudaMemAccessFlagsProtReadWrite;
+      (void)cudaMemPoolSetAccess(pool, &d, 1);
+    }
     if (cur >= 0) cudaSetDevice(cur);
   }
   (void)cudaGetLastError();
@@ -245,9 +299,15 @@ int ofl_stream_create(int dev, ofl_stream** out) {
   s->dev = dev;
   // non-blocking: never implicitly ordered with the legacy default stream
   e = cudaStreamCreateWithFlags(&s->cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->fence, cudaEventDisableTiming);
   if (e != cudaSuccess) {
+    if (s->cs) cudaStreamDestroy(s->cs);
     delete s;
     return cuda_error(e, "cudaStreamCreate");
+  }
+  {
+    std::lock_guard<std::mutex> l(g_streams_mu);
+    g_streams.insert(s);
   }
   *out = s;
   return OFL_OK;
@@ -255,6 +315,10 @@ int ofl_stream_create(int dev, ofl_stream** out) {
 
 int ofl_stream_destroy(ofl_stream* s) {
   OFL_CHECK_STREAM(s);
+  {
+    std::lock_guard<std::mutex> l(g_streams_mu);
+    g_streams.erase(s);
+  }
   use_device(s->dev);
   cudaStreamSynchronize(s->cs);
   {
@@ -262,6 +326,7 @@ int ofl_stream_destroy(ofl_stream* s) {
     s->markers.clear();
     if (s->scratch) cudaFree(s->scratch);
   }
+  if (s->fence) cudaEventDestroy(s->fence);
   cudaStreamDestroy(s->cs);
   delete s;
   return OFL_OK;
@@ -306,34 +371,62 @@ int ofl_ipc_close(int dev, void* dptr) {
   return OFL_OK;
 }
 
+static int oom(int dev, uint64_t bytes) {
+  return set_error(OFL_ERR_OOM, "cuda" + std::to_string(dev) + ": " + std::to_string(bytes) +
+                                    " bytes requested, allocation failed");
+}
+
 int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   if (bytes == 0) return set_error(OFL_ERR_BAD_ARGS, "buffer size must be positive");
+  if (dev < 0 || dev >= kMaxDev) return set_error(OFL_ERR_BAD_ARGS, "bad device ordinal");
+  cudaError_t e = use_device(dev);
+  if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+  std::lock_guard<std::mutex> g(g_zero_mu[dev]);
+  e = internal_stream(dev);
+  if (e == cudaSuccess) e = pool_setup(dev);
+  if (e != cudaSuccess) return cuda_error(e, "memory pool setup");
+  void* p = nullptr;
+  e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) return oom(dev, bytes);
+    return cuda_error(e, "cudaMallocAsync");
+  }
+  // zero-initialised like the reference's np.zeros storage (buffer.py:32);
+  // complete before any stream can see the pointer.
+  e = cudaMemsetAsync(p, 0, bytes, g_zero_stream[dev]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g_zero_stream[dev]);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(p, g_zero_stream[dev]);
+    return cuda_error(e, "zero fill");
+  }
+  *dptr = p;
+  return OFL_OK;
+}
+
+int ofl_malloc_shareable(int dev, uint64_t bytes, void** dptr) {
+  if (bytes == 0) return set_error(OFL_ERR_BAD_ARGS, "buffer size must be positive");
+  if (dev < 0 || dev >= kMaxDev) return set_error(OFL_ERR_BAD_ARGS, "bad device ordinal");
   cudaError_t e = use_device(dev);
   if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
   void* p = nullptr;
   e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
-    if (e == cudaErrorMemoryAllocation)
-      return set_error(OFL_ERR_OOM, "cuda" + std::to_string(dev) + ": " + std::to_string(bytes) +
-                                        " bytes requested, allocation failed");
+    if (e == cudaErrorMemoryAllocation) return oom(dev, bytes);
     return cuda_error(e, "cudaMalloc");
   }
-  // zero-initialised like the reference's np.zeros storage (buffer.py:32);
-  // ordered before any stream can see the pointer.
   std::lock_guard<std::mutex> g(g_zero_mu[dev]);
-  if (!g_zero_stream[dev]) {
-    e = cudaStreamCreateWithFlags(&g_zero_stream[dev], cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-      cudaFree(p);
-      return cuda_error(e, "cudaStreamCreate");
-    }
-  }
-  e = cudaMemsetAsync(p, 0, bytes, g_zero_stream[dev]);
+  e = internal_stream(dev);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, bytes, g_zero_stream[dev]);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g_zero_stream[dev]);
   if (e != cudaSuccess) {
     cudaFree(p);
     return cuda_error(e, "zero fill");
+  }
+  {
+    std::lock_guard<std::mutex> l(g_legacy_mu);
+    g_legacy.insert(p);
   }
   *dptr = p;
   return OFL_OK;
@@ -341,12 +434,39 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
 
 int ofl_free(int dev, void* dptr) {
   if (!dptr) return OFL_OK;
+  if (dev < 0 || dev >= kMaxDev) return set_error(OFL_ERR_BAD_ARGS, "bad device ordinal");
+  bool legacy;
+  {
+    std::lock_guard<std::mutex> l(g_legacy_mu);
+    legacy = g_legacy.erase(dptr) > 0;
+  }
   cudaError_t e = use_device(dev);
   if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
-  // cudaFree synchronises with in-flight work, so buffers drain before they
-  // are released (registry.py:104-109 semantics).
-  e = cudaFree(dptr);
-  if (e != cudaSuccess) return cuda_error(e, "cudaFree");
+  if (legacy) {
+    // shareable buffers: cudaFree synchronises with in-flight work, so they
+    // drain before they are released (registry.py:104-109 semantics)
+    e = cudaFree(dptr);
+    if (e != cudaSuccess) return cuda_error(e, "cudaFree");
+    return OFL_OK;
+  }
+  // ordered after the work enqueued so far on every live stream (any device
+  // may reach the buffer: peer copies, peer stores), without blocking them
+  std::lock_guard<std::mutex> g(g_free_mu[dev]);
+  if (!g_free_stream[dev]) {
+    e = cudaStreamCreateWithFlags(&g_free_stream[dev], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_error(e, "cudaStreamCreate");
+  }
+  {
+    std::lock_guard<std::mutex> l(g_streams_mu);
+    for (ofl_stream* s : g_streams) {
+      if (use_device(s->dev) != cudaSuccess) continue;
+      if (cudaEventRecord(s->fence, s->cs) == cudaSuccess)
+        (void)cudaStreamWaitEvent(g_free_stream[dev], s->fence, 0);
+    }
+  }
+  e = use_device(dev);
+  if (e == cudaSuccess) e = cudaFreeAsync(dptr, g_free_stream[dev]);
+  if (e != cudaSuccess) return cuda_error(e, "cudaFreeAsync");
   return OFL_OK;
 }
 

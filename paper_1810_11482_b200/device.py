@@ -201,10 +201,13 @@ class DeviceObject:
         return when_all([s.tail_token() for s in streams])
 
     # -- memory ----------------------------------------------------------------
-    def allocate(self, size: int) -> int:
+    def allocate(self, size: int, shareable: bool = False) -> int:
+        """Zero-filled device memory: from the stream-ordered pool, or (for
+        buffers exported to other processes through CUDA IPC) cudaMalloc."""
         lib = _native.load()
         p = ctypes.c_void_p()
-        status = lib.ofl_malloc(self.ordinal, size, ctypes.byref(p))
+        alloc = lib.ofl_malloc_shareable if shareable else lib.ofl_malloc
+        status = alloc(self.ordinal, size, ctypes.byref(p))
         if status:
             raise _native.error_for(status, f"{self.info.name}: allocation of {size} bytes")
         with self._lock:

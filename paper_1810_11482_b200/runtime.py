@@ -73,10 +73,12 @@ class CudaDispatch:
         return self._tokenized(lambda: self._device(device_gid).synchronize())
 
     # -- buffers -------------------------------------------------------------
-    def create_buffer(self, device_gid: GlobalId, size: int) -> CompletionToken:
+    def create_buffer(self, device_gid: GlobalId, size: int, shareable: bool = False) -> CompletionToken:
+        """`shareable` (extension): a buffer another process can map through
+        CUDA IPC (collectives.ProcessPeerGroup, bench.ProcessHeatSlabs)."""
         def start():
             device = self._device(device_gid)
-            buf = BufferObject(device, size)
+            buf = BufferObject(device, size, shareable)
             return make_ready(self._registry.register(ObjectKind.BUFFER, buf))
 
         return self._tokenized(start)

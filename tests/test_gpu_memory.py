@@ -1,0 +1,74 @@
+"""Stream-ordered device memory (csrc/ofl_runtime.cu: ofl_malloc / ofl_free
+on the device's memory pool): dropping a buffer neither stalls nor waits for
+other streams' in-flight work, and the memory is not reused before the work
+enqueued ahead of the free has finished."""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _long_heat(dev, stream: int, n: int = 1 << 27, steps: int = 3000):
+    """A kernel chain of ~50 ms on `stream` (heat builtin)."""
+    X, Y = dev.create_buffer(n * 8).get(), dev.create_buffer(n * 8).get()
+    X.enqueue_write(0, np.full(n, 0.5), stream).get()
+    prog = dev.create_builtin_program().get()
+    prog.build("heat").get()
+    tok = prog.run([X, Y, n, steps], "heat", (n // 256, 1, 1), (256, 1, 1), stream)
+    return tok, (X, Y)
+
+
+def test_free_does_not_stall_other_streams(rt, dev):
+    s1 = dev.create_stream()
+    tok, keep = _long_heat(dev, s1)
+    t0 = time.perf_counter()
+    for _ in range(4):
+        tmp = dev.create_buffer(64 << 20).get()  # allocate + zero fill on the internal stream
+        rt.registry.unregister(tmp.gid)          # last reference: ofl_free (stream-ordered)
+        del tmp
+    dt = time.perf_counter() - t0
+    # the free is enqueued behind the heat chain, not waited for
+    assert not tok.done(), "dropping buffers waited for another stream's kernel"
+    tok.get()
+    total = time.perf_counter() - t0
+    assert dt < 0.5 * total, (dt, total)
+
+
+def test_freed_memory_not_reused_before_prior_work(rt, dev):
+    """A buffer dropped while a kernel still writes it: a new allocation of
+    the same size must not see (or be clobbered by) that kernel's writes."""
+    s1, s2 = dev.create_stream(), dev.create_stream()
+    n = 1 << 26
+    for _ in range(3):
+        tok, (X, Y) = _long_heat(dev, s1, n=n, steps=400)
+        rt.registry.unregister(X.gid)
+        rt.registry.unregister(Y.gid)
+        del X, Y
+        Z = dev.create_buffer(n * 8).get()       # zero-filled, maybe the same pool memory
+        pattern = np.arange(n, dtype=np.float64)
+        Z.enqueue_write(0, pattern, s2).get()
+        tok.get()                                 # the heat chain has finished writing
+        got = np.frombuffer(Z.enqueue_read(0, n * 8, s2).get(), np.float64)
+        assert np.array_equal(got, pattern)
+
+
+def test_allocation_after_free_does_not_wait(rt, dev):
+    """Allocations go to their own stream: they never queue behind a free's
+    fence waits."""
+    s1 = dev.create_stream()
+    tok, keep = _long_heat(dev, s1)
+    tmp = dev.create_buffer(1 << 20).get()
+    rt.registry.unregister(tmp.gid)
+    del tmp
+    t0 = time.perf_counter()
+    fresh = dev.create_buffer(32 << 20).get()
+    dt = time.perf_counter() - t0
+    assert not tok.done()
+    assert fresh.enqueue_read(0, 16).get() == bytes(16)
+    tok.get()
+    assert dt < 0.05, dt
