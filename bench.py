@@ -799,18 +799,16 @@ def run_ours(args) -> None:
     dist.close()
 
 
-# Build-time / sweep switches that change which kernel variant runs; a
-# headline number must come from the shipped defaults.
-VARIANT_SWITCHES = ("OFL_HEAT_TB", "OFL_HEAT_R", "OFL_HEAT_FMA", "OFL_HEAT_KERNEL",
-                    "OFL_MANDEL_PERIOD", "OFL_MANDEL_FPCMP", "OFL_MANDEL_FUSED", "OFL_MANDEL_ILP",
-                    "OFL_REDUCE_CPS", "OFL_STENCIL_VARIANT", "OFL_STENCIL2D_VARIANT",
-                    "OFL_STREAM_VARIANT", "OFL_LIB", "OFL_NO_JIT")
+# Switches that change what runs (heat pass schedule, Mandelbrot without
+# cycle detection, a substitute library, no NVRTC): a headline number must
+# come from the shipped defaults.
+VARIANT_SWITCHES = ("OFL_HEAT_TB", "OFL_MANDEL_PERIOD", "OFL_LIB", "OFL_NO_JIT")
 
 
 def refuse_variant_switches(args) -> None:
     set_ = [k for k in VARIANT_SWITCHES if k in os.environ]
     if set_ and not args.allow_variants:
-        raise SystemExit(f"bench.py: refusing to run with kernel-variant switches set: {set_} "
+        raise SystemExit(f"bench.py: refusing to run with run-changing switches set: {set_} "
                          "(unset them, or pass --allow-variants for a sweep)")
 
 
@@ -848,7 +846,7 @@ def main(argv=None) -> None:
                     help="chain lengths K of the per-future overhead sweep (config 5)")
     ap.add_argument("--no-overhead", action="store_true")
     ap.add_argument("--allow-variants", action="store_true",
-                    help="permit OFL_* kernel-variant switches (sweeps only, never a headline)")
+                    help="permit OFL_* run-changing switches (sweeps only, never a headline)")
     ap.add_argument("--configs", default="heat,mandelbrot,dot",
                     help="BASELINE configs 2-4 measured after the headline (N=1 only); '' = none")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

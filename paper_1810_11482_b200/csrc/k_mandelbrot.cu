@@ -49,64 +49,9 @@ struct MandelArgs {
 // mag >= +0 and esc > 0 are finite, which the host guarantees by enabling it
 // only for esc in (0, 1e10] and a viewport inside [-1e10, 1e10]: then every
 // executed iteration starts from |z|^2 <= 1e10 and nothing overflows.
-template <bool INTCMP>
-__device__ __forceinline__ uint32_t escape_count(double cre, double cim, double esc,
-                                                 uint32_t max_iter) {
-  double zr = 0.0, zi = 0.0;
-  uint32_t count = 0;
-  const long long esc_bits = __double_as_longlong(esc);
-#pragma unroll 4
-  for (uint32_t i = 0; i < max_iter; ++i) {
-    const double zr2 = __dmul_rn(zr, zr);
-    const double zi2 = __dmul_rn(zi, zi);
-    const double mag = __dadd_rn(zr2, zi2);
-    if (INTCMP ? (__double_as_longlong(mag) > esc_bits) : (mag > esc)) break;
-    const double t = __dadd_rn(__dsub_rn(zr2, zi2), cre);
-    zi = __dadd_rn(__dmul_rn(__dmul_rn(2.0, zr), zi), cim);
-    zr = t;
-    ++count;
-  }
-  return count;
-}
-
-// Two pixels per thread, iterated in lock step (ILP 2 for the FP64 pipe,
-// branch-free body): an escaped pixel keeps iterating harmlessly but its
-// count is frozen; the loop ends when both have escaped or max_iter is hit.
-// Counts are exactly those of escape_count (same operations, same order).
-template <bool INTCMP>
-__device__ __forceinline__ void escape_count2(double cra, double cia, double crb, double cib,
-                                              double esc, uint32_t max_iter, uint32_t& na,
-                                              uint32_t& nb) {
-  double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-  uint32_t ca = 0, cb = 0;
-  bool la = true, lb = true;
-  const long long esc_bits = __double_as_longlong(esc);
-  for (uint32_t i = 0; i < max_iter; ++i) {
-    const double ar2 = __dmul_rn(ar, ar), ai2 = __dmul_rn(ai, ai);
-    const double br2 = __dmul_rn(br, br), bi2 = __dmul_rn(bi, bi);
-    const double ma = __dadd_rn(ar2, ai2), mb = __dadd_rn(br2, bi2);
-    if (INTCMP) {
-      la = la && !(__double_as_longlong(ma) > esc_bits);
-      lb = lb && !(__double_as_longlong(mb) > esc_bits);
-    } else {
-      la = la && !(ma > esc);
-      lb = lb && !(mb > esc);
-    }
-    if (!(la || lb)) break;
-    ca += la;
-    cb += lb;
-    const double ta = __dadd_rn(__dsub_rn(ar2, ai2), cra);
-    const double tb = __dadd_rn(__dsub_rn(br2, bi2), crb);
-    ai = __dadd_rn(__dmul_rn(__dmul_rn(2.0, ar), ai), cia);
-    bi = __dadd_rn(__dmul_rn(__dmul_rn(2.0, br), bi), cib);
-    ar = ta;
-    br = tb;
-  }
-  na = ca;
-  nb = cb;
-}
-
-// P pixels per thread in lock step (generalises escape_count2).
+// P pixels per thread in lock step (ILP P for the FP64 pipe, branch-free
+// body): an escaped pixel keeps iterating harmlessly but its count is
+// frozen; the loop ends when all have escaped or max_iter is hit.
 //
 // FUSED: zi' = (2*zr)*zi + cim is evaluated as fma(2, zr*zi, cim) — 7 DP ops
 // per iteration instead of 8.  Bit-identical to the reference whenever
@@ -260,81 +205,6 @@ __global__ void __launch_bounds__(kThreads, PERIOD ? 3 : 1) k_mandelbrotP(Mandel
   }
 }
 
-// ILP-2 variant of k_mandelbrot: a unit is 4 tiles of 8x4; lane l handles
-// the same tile position in tiles (k, k+1) — pixels 8 apart, which escape
-// at similar counts.
-template <bool INTCMP>
-__global__ void __launch_bounds__(kThreads) k_mandelbrot2(MandelArgs a, unsigned int* queue) {
-  const int lane = threadIdx.x & 31;
-  const double dre = __dsub_rn(a.re1, a.re0);
-  const double dim = __dsub_rn(a.im1, a.im0);
-  const double fw = (double)a.width, fh = (double)a.height;
-  while (true) {
-    unsigned int u = 0;
-    if (lane == 0) u = atomicAdd(queue, 1u);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if ((uint64_t)u >= a.units) break;
-#pragma unroll 1
-    for (int k = 0; k < kTilesPerUnit; k += 2) {
-      uint64_t at[2];
-      double cr[2], ci[2];
-      bool ok[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint64_t tile = (uint64_t)u * kTilesPerUnit + k + j;
-        const uint32_t ty = (uint32_t)(tile / a.tiles_x);
-        const uint32_t tx = (uint32_t)(tile % a.tiles_x);
-        const uint32_t px = tx * kTileW + (lane & (kTileW - 1));
-        const uint32_t r = ty * kTileH + (lane >> 3);
-        const uint32_t py = a.row_first + r * a.row_step;
-        const uint64_t gtid = (uint64_t)py * a.width + px;
-        ok[j] = r < a.rows && px < a.width && gtid < a.limit;
-        at[j] = a.compact ? (uint64_t)r * a.width + px : gtid;
-        cr[j] = __dadd_rn(a.re0, __ddiv_rn(__dmul_rn(__dadd_rn((double)px, 0.5), dre), fw));
-        ci[j] = __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
-      }
-      uint32_t n0, n1;
-      // a pixel outside the image runs with count frozen at 0 (never stored)
-      escape_count2<INTCMP>(ok[0] ? cr[0] : 1e3, ok[0] ? ci[0] : 0.0, ok[1] ? cr[1] : 1e3,
-                            ok[1] ? ci[1] : 0.0, a.esc, a.max_iter, n0, n1);
-      if (ok[0]) a.out[at[0]] = n0;
-      if (ok[1]) a.out[at[1]] = n1;
-    }
-  }
-}
-
-template <bool INTCMP>
-__global__ void __launch_bounds__(kThreads) k_mandelbrot(MandelArgs a, unsigned int* queue) {
-  const int lane = threadIdx.x & 31;
-  const double dre = __dsub_rn(a.re1, a.re0);
-  const double dim = __dsub_rn(a.im1, a.im0);
-  const double fw = (double)a.width, fh = (double)a.height;
-  while (true) {
-    unsigned int u = 0;
-    if (lane == 0) u = atomicAdd(queue, 1u);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if ((uint64_t)u >= a.units) break;
-#pragma unroll 1
-    for (int k = 0; k < kTilesPerUnit; ++k) {
-      const uint64_t tile = (uint64_t)u * kTilesPerUnit + k;
-      const uint32_t ty = (uint32_t)(tile / a.tiles_x);
-      const uint32_t tx = (uint32_t)(tile % a.tiles_x);
-      const uint32_t px = tx * kTileW + (lane & (kTileW - 1));
-      const uint32_t r = ty * kTileH + (lane >> 3);  // dense row index
-      if (r >= a.rows || px >= a.width) continue;
-      const uint32_t py = a.row_first + r * a.row_step;
-      const uint64_t gtid = (uint64_t)py * a.width + px;
-      if (gtid >= a.limit) continue;
-      const double cre =
-          __dadd_rn(a.re0, __ddiv_rn(__dmul_rn(__dadd_rn((double)px, 0.5), dre), fw));
-      const double cim =
-          __dadd_rn(a.im0, __ddiv_rn(__dmul_rn(__dadd_rn((double)py, 0.5), dim), fh));
-      const uint64_t at = a.compact ? (uint64_t)r * a.width + px : gtid;
-      a.out[at] = escape_count<INTCMP>(cre, cim, a.esc, a.max_iter);
-    }
-  }
-}
-
 }  // namespace
 
 extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint32_t height,
@@ -362,12 +232,11 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
     a.row_first = row_first;
     a.row_step = row_step;
     a.compact = compact;
-    static const int fused = [] {  // OFL_MANDEL_FUSED=0 disables (sweeps)
-      const char* e = getenv("OFL_MANDEL_FUSED");
-      return e ? atoi(e) != 0 : 1;
-    }();
-    a.fused = fused;
-    static const int period = [] {  // OFL_MANDEL_PERIOD=0 disables (sweeps)
+    a.fused = 1;  // fused zi update wherever its guard proves it bit-identical
+    // exact cycle detection on by default; OFL_MANDEL_PERIOD=0 runs the plain
+    // escape loop — the FP64-roofline measurement of config 3 (bench.py
+    // refuses the switch for headline runs)
+    static const int period = [] {
       const char* e = getenv("OFL_MANDEL_PERIOD");
       return e ? atoi(e) != 0 : 1;
     }();
@@ -393,39 +262,18 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       if (blocks > cap) blocks = cap;
       const double lim = 1e10;
       const bool intcmp = esc > 0.0 && esc <= lim && fabs(re0) <= lim && fabs(re1) <= lim &&
-                          fabs(im0) <= lim && fabs(im1) <= lim && getenv("OFL_MANDEL_FPCMP") == nullptr;
-      // pixels per thread in lock step (OFL_MANDEL_ILP 1/2/3/4); 4 measured
-      // fastest (profiles/r01_mandel_sweep.txt)
-      static const int ilp = [] {
-        const char* e = getenv("OFL_MANDEL_ILP");
-        return e ? atoi(e) : 4;
-      }();
-      if (ilp == 4) {
-        if (intcmp)
-          if (a.period)
-            k_mandelbrotP<true, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-          else
-            k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+                          fabs(im0) <= lim && fabs(im1) <= lim;
+      // 4 pixels per thread in lock step, measured fastest of 1/2/3/4
+      // (profiles/r01_mandel_sweep.txt; the other forms were removed)
+      if (intcmp)
+        if (a.period)
+          k_mandelbrotP<true, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
         else
-          if (a.period)
-            k_mandelbrotP<false, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-          else
-            k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-      } else if (ilp == 3) {  // the generic template at P=2
-        if (intcmp)
-          k_mandelbrotP<true, 2><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-        else
-          k_mandelbrotP<false, 2><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-      } else if (ilp == 2) {
-        if (intcmp)
-          k_mandelbrot2<true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-        else
-          k_mandelbrot2<false><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-      } else if (intcmp) {
-        k_mandelbrot<true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-      } else {
-        k_mandelbrot<false><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
-      }
+          k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      else if (a.period)
+        k_mandelbrotP<false, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+      else
+        k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       e = cudaPeekAtLastError();
       if (e != cudaSuccess) return ofl::cuda_error(e, "mandelbrot launch");
       ofl::count_launch();

@@ -204,14 +204,8 @@ __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ 
 // (profiles/r01_reduce_grid.txt): the per-CTA atomic ticket and the last
 // CTA's fold over ~10^5 partials cost more than the tail it balances.  CTAs
 // per SM per kernel from the read-bandwidth sweep (scripts/probes/
-// read_bw_probe.cu, scripts/reduce_sweep.sh); OFL_REDUCE_CPS overrides.
-int grid_for(ofl_stream* s, uint64_t vec_units, int unroll, int cps) {
-  static const int env_cps = [] {
-    const char* e = getenv("OFL_REDUCE_CPS");
-    return e ? atoi(e) : 0;
-  }();
-  if (env_cps >= 1 && env_cps <= 4) cps = env_cps;
-  uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
+// read_bw_probe.cu, scripts/reduce_sweep.sh).
+int grid_for(ofl_stream* s, uint64_t vec_units, int unroll, int cps) {  uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
   uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * cps;
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   if (blocks > cap) blocks = cap;

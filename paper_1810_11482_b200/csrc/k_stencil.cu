@@ -10,16 +10,16 @@
 // operation is a separate IEEE operation).  Items are independent, so the
 // parallel order is free.
 //
-// Single step (k_stencil): each thread owns an aligned pair of cells loaded
-// as one 128-bit vector; the outer neighbours come from the adjacent lanes by
-// warp shuffle, so every cell is read from HBM once: 16 B/cell.
+// Single step (k_stencil_smem): each thread owns aligned pairs of cells
+// loaded as 128-bit vectors and staged in shared memory with the two cells
+// just outside the CTA's range, so every cell is read from HBM once: 16 B/cell.
 //
 // Temporal blocking (k_heat_pipe, below): a warp holds a tile of cells plus
 // a halo of `tb` cells each side in registers, advances it `tb` steps (the
 // valid region shrinks by one cell per side per step), and writes the
 // centre back: 16 B/cell per `tb` steps instead of per step.  Global
 // endpoints are fixed points of the update, exactly as stencil.k.
-#include <cstdlib>
+
 
 #include "ofl_internal.h"
 
@@ -41,58 +41,6 @@ __device__ __forceinline__ double point(double l, double c, double r) {
 
 // m  = number of items that execute (min(n, grid*block of the .k launch))
 // hi = highest readable x index = min(m, n-1)
-// One-shot tiles (as the STREAM kernels: the block scheduler balances many
-// CTAs better than a persistent grid): a CTA of T threads covers U*T cell
-// pairs; thread t owns pairs base + t + u*T (cells 2j, 2j+1), so every load
-// instruction of a warp is one contiguous 512-byte run.  kPDL: programmatic
-// dependent launch (see k_stream.cu) for back-to-back steps.
-template <int T, int U, bool kPDL>
-__global__ void __launch_bounds__(T) k_stencil(const double* __restrict__ x,
-                                               double* __restrict__ y, uint64_t n, uint64_t m) {
-  if constexpr (kPDL) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-  }
-  const int lane = threadIdx.x & 31;
-  const uint64_t hi = (m < n - 1) ? m : n - 1;
-  double edge[U];
-  double2 v[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint64_t j = (uint64_t)blockIdx.x * (T * U) + (uint64_t)u * T + threadIdx.x;
-    const uint64_t lo = 2 * j;
-    // the warp-edge neighbours are loaded together with the main vectors, so
-    // a warp waits for one memory latency, not two
-    edge[u] = 0.0;
-    if (lane == 0 && lo >= 1 && lo - 1 <= hi) edge[u] = x[lo - 1];
-    if (lane == 31 && lo + 2 <= hi) edge[u] = x[lo + 2];
-    v[u] = make_double2(0.0, 0.0);
-    if (lo + 1 <= hi) {
-      v[u] = ld_nc(reinterpret_cast<const double2*>(x) + j);
-    } else if (lo <= hi) {
-      v[u].x = x[lo];
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const uint64_t j = (uint64_t)blockIdx.x * (T * U) + (uint64_t)u * T + threadIdx.x;
-    const uint64_t lo = 2 * j;
-    double left = __shfl_up_sync(0xffffffffu, v[u].y, 1);
-    double right = __shfl_down_sync(0xffffffffu, v[u].x, 1);
-    if (lane == 0) left = edge[u];
-    if (lane == 31) right = edge[u];
-    if (lo < m) {
-      const double r0 = (lo == 0 || lo == n - 1) ? v[u].x : point(left, v[u].x, v[u].y);
-      if (lo + 1 < m) {
-        const double r1 = (lo + 1 == n - 1) ? v[u].y : point(v[u].x, v[u].y, right);
-        __stcs(reinterpret_cast<double2*>(y) + j, make_double2(r0, r1));
-      } else {
-        y[lo] = r0;
-      }
-    }
-  }
-}
-
 // Shared-memory form: the CTA's U*T pairs are staged once in shared memory
 // with the two cells just outside the CTA's range (loaded by threads 0 and
 // T-1), so each cell's outer neighbours come from shared memory instead of a
@@ -161,49 +109,12 @@ void launch_stencil_smem(cudaStream_t cs, const double* x, double* y, uint64_t n
   cudaLaunchKernelEx(&cfg, k_stencil_smem<T, U, true>, x, y, n, m);
 }
 
-// single-step launch shape (OFL_STENCIL_VARIANT, sweeps; 2^28 cells, back
-// to back): 0 = shared-memory staging, 256 threads x 4 pairs, PDL (default:
-// 621 us/step, 6.91 TB/s — copy speed); shuffle form 1 = 256 x 1 (the first
-// version, 713 us), 2 = 512 x 1 + PDL (742), 3 = 256 x 4 + PDL (770),
-// 7 = 512 x 2 + PDL (706); smem form 4 = 512 x 2 (630), 5 = 512 x 1 (786)
-int stencil_variant() {
-  static int v = [] {
-    const char* e = getenv("OFL_STENCIL_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-template <int T, int U, bool kPDL>
-void launch_stencil_t(cudaStream_t cs, const double* x, double* y, uint64_t n, uint64_t m) {
-  const uint64_t npairs = (m + 1) >> 1;
-  const unsigned blocks = (unsigned)((npairs + (uint64_t)T * U - 1) / ((uint64_t)T * U));
-  if (!kPDL) {
-    k_stencil<T, U, false><<<blocks, T, 0, cs>>>(x, y, n, m);
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(T);
-  cfg.stream = cs;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_stencil<T, U, true>, x, y, n, m);
-}
-
+// One stencil step, the shape measured fastest on B200 (2^28 cells back to
+// back: 621 us/step, 6.91 TB/s = copy speed; the warp-shuffle form with
+// per-warp edge loads and other launch shapes measured 630-786 us and were
+// removed, profiles/r01_stencil_ncu.txt).
 void launch_stencil(cudaStream_t cs, const double* x, double* y, uint64_t n, uint64_t m) {
-  switch (stencil_variant()) {
-    case 1: launch_stencil_t<256, 1, false>(cs, x, y, n, m); break;
-    case 2: launch_stencil_t<512, 1, true>(cs, x, y, n, m); break;
-    case 3: launch_stencil_t<256, 4, true>(cs, x, y, n, m); break;
-    case 4: launch_stencil_smem<512, 2>(cs, x, y, n, m); break;
-    case 5: launch_stencil_smem<512, 1>(cs, x, y, n, m); break;
-    case 7: launch_stencil_t<512, 2, true>(cs, x, y, n, m); break;
-    default: launch_stencil_smem<256, 4>(cs, x, y, n, m); break;
-  }
+  launch_stencil_smem<256, 4>(cs, x, y, n, m);
 }
 
 // ---------------------------------------------------------------- heat ---

@@ -1,7 +1,7 @@
 """Run one workload a few times through the public API — the target of an
 ncu capture (`ncu --set full -k regex:<kernel> -c 1 ... python
 scripts/profile_kernels.py <workload>`).  Workloads at BASELINE sizes:
-triad (2^25 f64), stencil (2^28 f64, one step), heat (2^28, 64 steps),
+triad (2^25 f64), stencil (2^28 f64, one step), heat (2^28, 1000 steps),
 mandel (7680x4320 @2000), dot (2^31 f32), sum (2^28 u32)."""
 
 import os
@@ -62,7 +62,8 @@ def main(which: str, reps: int = 3):
             else:
                 p = d.create_builtin_program().get()
                 p.build("heat").get()
-                p.run([X, Y, n, 64 * reps], "heat", (n // 256, 1, 1), (256, 1, 1))
+                # config 2's schedule: 1000 steps = 12 passes of ~83 steps
+                p.run([X, Y, n, 1000], "heat", (n // 256, 1, 1), (256, 1, 1))
         elif which == "mandel":
             w, h = 7680, 4320
             O = d.create_buffer(w * h * 4).get()

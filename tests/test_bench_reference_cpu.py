@@ -53,7 +53,7 @@ def test_gpus_flag_spawns_ranks_without_torchrun():
 
 def test_variant_switches_refused():
     r = _run({"WORLD_SIZE": "1", "RANK": "0", "OFL_HEAT_TB": "8"})
-    assert r.returncode != 0 and "kernel-variant switches" in (r.stderr + r.stdout)
+    assert r.returncode != 0 and "run-changing switches" in (r.stderr + r.stdout)
 
 
 def test_world_size_must_match_gpus():

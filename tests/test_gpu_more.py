@@ -227,36 +227,6 @@ def test_heat2d_fused_row_slabs(parts, w, h, steps):
     assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
 
 
-TMA2D_SCRIPT = r"""
-import sys
-sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
-import numpy as np
-import oracle
-from flows import device_stencil2d
-from paper_1810_11482_b200 import Runtime
-with Runtime(devices=[0]) as rt:
-    dev = rt.get_all_devices().get()[0]
-    for w, h in ((64, 32), (130, 67), (2, 5), (4096, 97), (66, 1)):
-        x = np.random.default_rng(w + h).random(w * h)
-        got = np.frombuffer(device_stencil2d(dev, x, w, h, steps=3), np.float64)
-        assert np.array_equal(got, oracle.heat2d(x, w, h, 3)), (w, h)
-print("tma ok")
-"""
-
-
-def test_stencil2d_tma_variant_bitexact():
-    """The TMA-staged 2-D kernel (sweep variant 5) against the oracle, in a
-    subprocess because the variant is chosen once per process."""
-    import subprocess
-    import sys
-
-    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, OFL_STENCIL2D_VARIANT="5")
-    r = subprocess.run([sys.executable, "-c", TMA2D_SCRIPT, repo], capture_output=True, text=True,
-                       timeout=300, env=env)
-    assert r.stdout.strip().endswith("tma ok"), r.stdout[-500:] + r.stderr[-1500:]
-
-
 PLAIN_MANDEL_SCRIPT = r"""
 import sys, hashlib, json
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
