@@ -122,6 +122,8 @@ def main():
                 "result": got, "oracle": total, "rel_err": abs(got - total) / abs(total),
                 "within_1e-5": abs(got - total) <= 1e-5 * abs(total),
             }), flush=True)
+        if not abs(got - total) <= 1e-12 * abs(total):
+            raise SystemExit(f"rank {rank}: dot parity FAILED ({got} vs {total})")
         if comm is not None:
             comm.close()
         if group is not None:

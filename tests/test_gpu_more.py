@@ -299,7 +299,8 @@ n = 3_000_001
 rng = np.random.default_rng(7)
 a = rng.random(n, dtype=np.float32); b = rng.random(n, dtype=np.float32)
 lo, hi = n * rank // world, n * (rank + 1) // world
-with Runtime(devices=[0]) as rt:
+import os
+with Runtime(devices=[int(os.environ.get("TEST_DEVICE", "0"))]) as rt:
     dev = rt.get_all_devices().get()[0]
     A = dev.create_buffer((hi - lo) * 4).get(); B = dev.create_buffer((hi - lo) * 4).get()
     R = dev.create_buffer(8).get()
@@ -371,14 +372,16 @@ from paper_1810_11482_b200 import Runtime
 from paper_1810_11482_b200.bench.harness import ProcessHeatSlabs
 dist.init_process_group("gloo")
 rank = dist.get_rank()
-x = np.random.default_rng(3).random(40_001)
-with Runtime(devices=[0]) as rt:
+x = np.random.default_rng(3).random(int(sys.argv[2]) if len(sys.argv) > 2 else 40_001)
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 45
+import os
+with Runtime(devices=[int(os.environ.get("TEST_DEVICE", "0"))]) as rt:
     dev = rt.get_all_devices().get()[0]
-    slabs = ProcessHeatSlabs(rt, dev, x, halo=16)
-    slabs.run(45).get(timeout=120)
+    slabs = ProcessHeatSlabs(rt, dev, x, halo=16 if x.size < 100_000 else 96)
+    slabs.run(steps).get(timeout=120)
     got = slabs.gather()
     slabs.close()
-assert got.tobytes() == oracle.heat(x, 45, threads=0).tobytes()
+assert got.tobytes() == oracle.heat(x, steps, threads=0).tobytes()
 print(f"rank {rank} heat ipc ok", flush=True)
 """
 
