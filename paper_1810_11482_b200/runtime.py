@@ -228,6 +228,8 @@ class Runtime:
         self.registry = Registry(locality_id)
         self.local = CudaDispatch(self.registry)
         self._devices: list[tuple[GlobalId, DeviceObject]] = []
+        self._connections: dict = {}      # locality id -> transport.RemoteLocality
+        self._remote_devices: dict = {}   # locality id -> [(gid, DeviceInfo)]
         self._closed = False
         for i, o in enumerate(ordinals):
             name = device_names[i] if device_names else None
@@ -236,9 +238,15 @@ class Runtime:
             self._devices.append((gid, obj))
 
     def dispatch(self, gid: GlobalId):
+        """The dispatch serving gid: this process's CUDA devices, or the
+        proxy of the connected locality that minted it (reference
+        runtime.py:178-184)."""
         if gid.locality_id == self.registry.self_locality_id:
             return self.local
-        raise UnknownGidError(f"{gid} names an unknown locality")
+        proxy = self._connections.get(gid.locality_id)
+        if proxy is None:
+            raise UnknownGidError(f"{gid} names an unknown locality")
+        return proxy
 
     def local_program(self, gid: GlobalId):
         """(registry, generation, weakref to the ProgramObject) for a program
@@ -268,10 +276,14 @@ class Runtime:
             return None
 
     def get_all_devices(self, major: int = 0, minor: int = 0) -> CompletionToken:
-        """Every device with capability >= (major, minor), in ordinal order."""
-        return make_ready(
-            [DeviceHandle(g, o.info, self) for g, o in self._devices if o.info.meets(major, minor)]
-        )
+        """Every device with capability >= (major, minor): this process's in
+        ordinal order, then connected localities' ordered by locality id
+        (reference runtime.py:188-200)."""
+        out = [DeviceHandle(g, o.info, self) for g, o in self._devices if o.info.meets(major, minor)]
+        for lid in sorted(self._remote_devices):
+            out.extend(DeviceHandle(g, i, self) for g, i in self._remote_devices[lid]
+                       if i.meets(major, minor))
+        return make_ready(out)
 
     def local_device_table(self) -> list[tuple[GlobalId, DeviceInfo]]:
         return [(g, o.info) for g, o in self._devices]
@@ -286,12 +298,28 @@ class Runtime:
         return None
 
     def connect(self, address: str) -> LocalityInfo:
-        raise BadArgsError("remote localities are not supported by the CUDA runtime")
+        """Connect to a daemon at ``host:port`` (this package's ``serve`` or
+        the reference's ``offloadd``); its devices join discovery and its
+        gids dispatch to the connection (reference runtime.py:204-216)."""
+        from . import transport
+
+        proxy = transport.connect(address)
+        info = LocalityInfo(proxy.locality_id, address)
+        try:
+            self.registry.add_locality(info, proxy)
+        except ValueError:
+            proxy.close()
+            raise
+        self._connections[proxy.locality_id] = proxy
+        self._remote_devices[proxy.locality_id] = proxy.devices
+        return info
 
     def close(self) -> None:
         if self._closed:
             return
         self._closed = True
+        for proxy in self._connections.values():
+            proxy.close()
         for _, obj in self._devices:
             obj.close()
 

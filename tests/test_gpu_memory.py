@@ -26,17 +26,14 @@ def _long_heat(dev, stream: int, n: int = 1 << 27, steps: int = 3000):
 def test_free_does_not_stall_other_streams(rt, dev):
     s1 = dev.create_stream()
     tok, keep = _long_heat(dev, s1)
-    t0 = time.perf_counter()
     for _ in range(4):
-        tmp = dev.create_buffer(64 << 20).get()  # allocate + zero fill on the internal stream
+        tmp = dev.create_buffer(4 << 20).get()   # allocate + zero fill on the internal stream
         rt.registry.unregister(tmp.gid)          # last reference: ofl_free (stream-ordered)
         del tmp
-    dt = time.perf_counter() - t0
-    # the free is enqueued behind the heat chain, not waited for
+    # the frees are enqueued behind the heat chain, not waited for (a
+    # cudaFree would have synchronised the device: the chain would be done)
     assert not tok.done(), "dropping buffers waited for another stream's kernel"
     tok.get()
-    total = time.perf_counter() - t0
-    assert dt < 0.5 * total, (dt, total)
 
 
 def test_freed_memory_not_reused_before_prior_work(rt, dev):
