@@ -157,6 +157,13 @@ class Dist:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
     def gather(self, obj) -> list:
         if self.dist is None:
             return [obj]
@@ -597,6 +604,172 @@ def dev_ordinal(rt) -> int:
     return rt.device_objects()[0].ordinal
 
 
+def multi_heat(rt, dev, lib, D, rank: int, world: int) -> dict:
+    """Config 2 across the ranks (strong scaling): 2^28 cells x 1000 steps
+    in slabs, one process per GPU, the halo exchange fused into each pass
+    as peer stores through CUDA IPC (bench.ProcessHeatSlabs).  Each rank
+    generates only its slab of the reference input (PCG64 advanced to the
+    slab's first cell).  Parity: rank 0 hashes the owned cells of every rank
+    in order and compares with the reference's sha256."""
+    import hashlib
+
+    import numpy as np
+
+    from paper_1810_11482_b200.bench import decomp
+    from paper_1810_11482_b200.bench.harness import ProcessHeatSlabs
+
+    n, steps, halo = 1 << 28, 1000, 96
+    sl = decomp.slabs(n, world, halo)[rank]
+    bg = np.random.PCG64(20180214)
+    bg.advance(sl.start)
+    x_local = np.random.Generator(bg).random(sl.length)
+    slabs = ProcessHeatSlabs(rt, dev, x_local, halo=halo, n=n)
+    st = rt.device_objects()[0].stream(0)
+    t = EventTimer(lib, st, dev_ordinal(rt))
+
+    def one(k: int) -> float:
+        slabs.reset(x_local)
+        D.barrier()
+        t.start()
+        slabs.run(k).get(timeout=300)
+        ms = t.stop()
+        D.barrier()
+        return D.max(ms)
+
+    one(halo)  # warm-up: IPC mappings, first launches
+    times = [one(steps) for _ in range(2)]
+    mine = slabs.owned()
+    digest = None
+    dd, torch = D.dist, D.torch
+    if rank == 0:
+        h = hashlib.sha256(mine)
+        for r in range(1, world):
+            size = torch.zeros(1, dtype=torch.int64)
+            dd.recv(size, src=r)
+            buf = torch.empty(int(size.item()), dtype=torch.uint8)
+            dd.recv(buf, src=r)
+            h.update(buf.numpy().tobytes())
+        digest = h.hexdigest()
+    else:
+        dd.send(torch.tensor([len(mine)], dtype=torch.int64), dst=0)
+        dd.send(torch.frombuffer(bytearray(mine), dtype=torch.uint8), dst=0)
+    slabs.close()
+    ref = next((c for c in _golden("golden_long.json").get("heat", [])
+                if c["n"] == n and c["steps"] == steps), None)
+    ms = min(times)
+    useful = 2.0 * n * steps
+    fp64 = fp64_peak_ops(lib, st)
+    return {
+        "workload": f"heat 2^28 fp64 x 1000 steps (BASELINE config 2) over {world} GPUs, one "
+                    "process each, slabs with the halo exchange fused into the pass (peer stores "
+                    "via CUDA IPC, halo 96)",
+        "scaling": "strong", "n_gpus": world, "kernel_ms_max_over_ranks": round(ms, 3),
+        "frac_fp64_per_gpu": round(useful / (ms * 1e-3) / (fp64 * world), 4) if fp64 else None,
+        "parity": None if rank else ("bit-exact vs reference (golden_long.json)"
+                                     if ref and digest == ref["sha256"] else "MISMATCH vs reference"),
+    }
+
+
+def multi_dot(rt, dev, lib, D, rank: int, world: int) -> dict:
+    """Config 4 across the ranks (strong scaling): 2^31 fp32 elements in
+    contiguous shards, the cross-GPU sum fused into the reduction kernel over
+    CUDA-IPC-mapped peer memory (collectives.ProcessPeerGroup)."""
+    import numpy as np
+
+    import oracle
+    from paper_1810_11482_b200.bench import decomp
+    from paper_1810_11482_b200.collectives import ProcessPeerGroup
+
+    n = 1 << 31
+    lo, hi = decomp.shard_bounds(n, world)[rank:rank + 2]
+    m = hi - lo
+    rng = np.random.default_rng(20180214 + rank)
+    a = rng.random(m, dtype=np.float32)
+    b = rng.random(m, dtype=np.float32)
+    A, B, R = dev.create_buffer(m * 4).get(), dev.create_buffer(m * 4).get(), dev.create_buffer(8).get()
+    A.enqueue_write(0, a)
+    B.enqueue_write(0, b).get()
+    part = oracle.dot_f32(a, b, threads=0)
+    del a, b
+    grp = ProcessPeerGroup(rt, dev)
+    st = rt.device_objects()[0].stream(0)
+    for _ in range(3):
+        grp.dot_f32(A, B, R, m)
+    dev.synchronize().get()
+    t = EventTimer(lib, st, dev_ordinal(rt))
+    K = 10
+    D.barrier()
+    t.start()
+    for _ in range(K):
+        grp.dot_f32(A, B, R, m)
+    ms = D.max(t.stop() / K)
+    got = float(np.frombuffer(R.enqueue_read(0, 8).get(), np.float64)[0])
+    total = D.sum(part)
+    D.barrier()
+    grp.close()
+    rel = abs(got - total) / abs(total)
+    peak, _ = hbm_peak()
+    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+    return {
+        "workload": f"dot fp32 N=2^31 (BASELINE config 4) over {world} GPUs, one process each, "
+                    "partials exchanged inside the reduction kernel over peer memory",
+        "scaling": "strong", "n_gpus": world, "kernel_ms_max_over_ranks": round(ms, 4),
+        "gbs_whole_job": round(gbs, 1), "frac_hbm_per_gpu": round(gbs / (peak * world), 4),
+        "rel_err_vs_oracle": rel,
+        "parity": "within 1e-12 (tolerance 1e-5)" if rel <= 1e-12 else
+                  ("within 1e-5" if rel <= 1e-5 else "MISMATCH"),
+    }
+
+
+def multi_mandelbrot(rt, dev, lib, D, rank: int, world: int) -> dict:
+    """Config 3 across the ranks: cyclic rows (row r -> rank r mod world),
+    8 chunks per rank read straight into a pinned image; the images are
+    summed to rank 0 (disjoint rows) and hashed against the reference's."""
+    import hashlib
+
+    from paper_1810_11482_b200 import when_all
+    from paper_1810_11482_b200.bench.harness import MandelbrotTiles
+
+    w, h, it = 7680, 4320, 2000
+    tiles = MandelbrotTiles([dev], w, h, it, chunks=8, shard=(rank, world))
+    tiles.image[:] = 0
+    when_all(tiles.enqueue()).get()
+    wall = []
+    for _ in range(5):
+        D.barrier()
+        t0 = time.perf_counter()
+        when_all(tiles.enqueue()).get()
+        wall.append(D.max(time.perf_counter() - t0))
+    dd, torch = D.dist, D.torch
+    img = torch.from_numpy(tiles.image.view("int32").copy())
+    dd.reduce(img, dst=0, op=dd.ReduceOp.SUM)
+    ref = next((c for c in _golden("golden.json").get("mandelbrot", [])
+                if c["width"] == w and c["height"] == h and c["max_iter"] == it), None)
+    ok = rank == 0 and ref is not None and \
+        hashlib.sha256(img.numpy().tobytes()).hexdigest() == ref["sha256"]
+    return {
+        "workload": f"Mandelbrot 7680x4320 @2000 (BASELINE config 3) over {world} GPUs, one "
+                    "process each, cyclic rows into each rank's pinned image",
+        "scaling": "strong", "n_gpus": world,
+        "e2e_ms_max_over_ranks": round(min(wall) * 1e3, 3),
+        "parity": None if rank else ("bit-exact vs reference sha256" if ok else "MISMATCH"),
+    }
+
+
+def run_multi_configs(rt, dev, lib, D, rank: int, world: int, names) -> dict:
+    out = {}
+    for name in names:
+        t0 = time.time()
+        fn = {"heat": multi_heat, "dot": multi_dot, "mandelbrot": multi_mandelbrot}[name]
+        try:
+            out[name] = fn(rt, dev, lib, D, rank, world)
+        except Exception as exc:  # noqa: BLE001 - reported; the headline still prints
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        out[name]["wall_s"] = round(time.time() - t0, 1)
+        dev.synchronize().get()
+    return out
+
+
 def run_configs(rt, dev, lib, names) -> dict:
     out = {}
     st = rt.device_objects()[0].stream(0)
@@ -732,8 +905,13 @@ def run_ours(args) -> None:
         overhead = OverheadBench(dev, rt).sweep(ks)
 
     configs = None
-    if rank == 0 and world == 1 and args.configs:
-        configs = run_configs(rt, dev, lib, [c for c in args.configs.split(",") if c])
+    names = [c for c in args.configs.split(",") if c]
+    if rank == 0 and world == 1 and names:
+        configs = run_configs(rt, dev, lib, names)
+        configs["overhead"] = overhead
+    elif world > 1 and names and (not oversubscribed or args.force_multi):
+        # configs 2-4 across the ranks (every rank takes part; rank 0 reports)
+        configs = run_multi_configs(rt, dev, lib, dist, rank, world, names)
         configs["overhead"] = overhead
 
     cpu = None
@@ -845,6 +1023,8 @@ def main(argv=None) -> None:
     ap.add_argument("--overhead-ks", default="1,10,100,1000,10000,100000",
                     help="chain lengths K of the per-future overhead sweep (config 5)")
     ap.add_argument("--no-overhead", action="store_true")
+    ap.add_argument("--force-multi", action="store_true",
+                    help="run the multi-GPU configs even with more ranks than GPUs (testing)")
     ap.add_argument("--allow-variants", action="store_true",
                     help="permit OFL_* run-changing switches (sweeps only, never a headline)")
     ap.add_argument("--configs", default="heat,mandelbrot,dot",

@@ -360,12 +360,21 @@ class MandelbrotTiles:
 
     def __init__(self, devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
                  viewport=VIEWPORT, esc: float = 4.0, stream: int = 0, chunks: int = 1,
-                 interleave: bool = True):
+                 interleave: bool = True, shard: Optional[tuple] = None):
+        """``shard=(index, count)``: one process per GPU — the (single) device
+        computes the rows of part `index` of `count` into its image; the
+        other parts' rows are left untouched (another process owns them)."""
         self.devices = list(devices)
         self.width, self.height, self.max_iter = width, height, max_iter
         self.viewport, self.esc = viewport, esc
+        if shard is not None:
+            if len(self.devices) != 1 or not 0 <= shard[0] < shard[1]:
+                raise BadArgsError("a shard is one device's part index < part count")
+            self._total, self._index = shard[1], [shard[0]]
+        else:
+            self._total, self._index = len(self.devices), list(range(len(self.devices)))
         G = len(self.devices)
-        self.rows = [len(decomp.cyclic_rows(height, G, g)) for g in range(G)]
+        self.rows = [len(decomp.cyclic_rows(height, self._total, self._index[g])) for g in range(G)]
         self.progs = [_builtin(d, "mandelbrot_rows") for d in self.devices]
         self.streams, self.parts = [], []
         self._reads = {}  # (device, chunk) -> ticket of the chunk's last read
@@ -393,10 +402,12 @@ class MandelbrotTiles:
         from ..completion import DeviceToken
 
         G = len(self.devices)
+        P = self._total  # parts of the cyclic row split
         re0, re1, im0, im1 = self.viewport
         w = self.width
         toks = []
         for g in range(G):
+            part = self._index[g]
             sids = self.streams[g]
             copy = sids[-1]
             split = len(sids) > 1
@@ -412,10 +423,10 @@ class MandelbrotTiles:
                     if prev:  # WAR: the last read of this chunk's buffer
                         _native.check(s_compute.lib.ofl_stream_wait(s_compute.ptr, s_copy.ptr,
                                                                     prev), "chunk ordering")
-                first = g + k0 * G  # image row of the chunk's first row
-                items = (first + (cnt - 1) * step * G + 1) * w  # through its last row
+                first = part + k0 * P  # image row of the chunk's first row
+                items = (first + (cnt - 1) * step * P + 1) * w  # through its last row
                 run = self.progs[g].run([buf, w, self.height, re0, re1, im0, im1, self.esc,
-                                         self.max_iter, first, step * G], "mandelbrot_rows",
+                                         self.max_iter, first, step * P], "mandelbrot_rows",
                                         (items // w, 1, 1), (w, 1, 1), compute)  # exactly items
                 if split:
                     if type(run) is not DeviceToken:
@@ -424,7 +435,7 @@ class MandelbrotTiles:
                     _native.check(s_copy.lib.ofl_stream_wait(s_copy.ptr, s_compute.ptr,
                                                              run._ticket), "chunk ordering")
                 read = buf.enqueue_read_rows_into(0, self.image, w * 4, cnt, first * w * 4,
-                                                  step * G * w * 4, copy)
+                                                  step * P * w * 4, copy)
                 if split and type(read) is DeviceToken:
                     self._reads[(g, i)] = read._ticket
                 toks.append(read)
@@ -599,7 +610,11 @@ class ProcessHeatSlabs:
     (ofl_heat_slab over the IPC mappings), (3) a one-thread kernel that
     publishes this rank's counter — no host synchronisation per exchange."""
 
-    def __init__(self, rt, device: DeviceHandle, x: np.ndarray, halo: int = 64, group=None):
+    def __init__(self, rt, device: DeviceHandle, x: np.ndarray, halo: int = 64, group=None,
+                 n: Optional[int] = None):
+        """x: the whole vector, or (with ``n`` = the global length) only this
+        rank's slab — its ``decomp.slabs(n, world, halo)[rank]`` cells, ghosts
+        included — so no rank has to hold the whole field."""
         import ctypes
 
         import torch.distributed as dist
@@ -610,14 +625,20 @@ class ProcessHeatSlabs:
             raise BadArgsError("halo must be 1..128")
         lib = _native.load()
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.group, self.halo, self.n = group, halo, x.size
+        total = x.size if n is None else int(n)
+        self.group, self.halo, self.n = group, halo, total
         try:
-            self.layout = decomp.slabs(x.size, self.world, halo)
+            self.layout = decomp.slabs(total, self.world, halo)
         except ValueError as exc:
             raise BadArgsError(str(exc)) from None
-        self.bounds = decomp.shard_bounds(x.size, self.world)
+        self.bounds = decomp.shard_bounds(total, self.world)
         sl = self.layout[self.rank]
-        local = np.ascontiguousarray(np.asarray(x, dtype=np.float64)[sl.start : sl.start + sl.length])
+        if n is None:
+            local = np.ascontiguousarray(np.asarray(x, dtype=np.float64)[sl.start : sl.start + sl.length])
+        else:
+            local = np.ascontiguousarray(x, dtype=np.float64)
+            if local.size != sl.length:
+                raise BadArgsError(f"rank {self.rank}'s slab has {sl.length} cells, got {local.size}")
         self.bufs = [device.create_buffer(local.nbytes, shareable=True).get() for _ in range(2)]
         self.bufs[0].enqueue_write(0, local.tobytes())
         self.block = device.create_buffer(64, shareable=True).get()  # [0] counter, [8] status
@@ -684,6 +705,23 @@ class ProcessHeatSlabs:
             self.cur = nxt
             done += k
         return st.token(ticket.value) if steps else None
+
+    def reset(self, local: np.ndarray) -> None:
+        """Restart from `local` (this rank's slab cells, ghosts included).
+        Call between runs, when no rank has a pass in flight (e.g. after a
+        barrier): it rewrites the buffer the next pass reads."""
+        self.bufs[0].enqueue_write(0, np.ascontiguousarray(local, dtype=np.float64))
+        self.cur = 0
+
+    def owned(self) -> bytes:
+        """This rank's owned cells of the current state (raises if a gate
+        timed out waiting for a neighbour)."""
+        sl = self.layout[self.rank]
+        mine = self.bufs[self.cur].enqueue_read(sl.left * 8, sl.owned * 8).get()
+        status = np.frombuffer(self.block.enqueue_read(8, 8).get(), np.uint64)[0]
+        if status:
+            raise RuntimeError("heat slab gate timed out waiting for a neighbour")
+        return mine
 
     def gather(self) -> np.ndarray:
         """The whole vector on every rank (host all-gather of the owned cells)."""
