@@ -549,8 +549,10 @@ def config_mandelbrot(rt, dev, lib, fp64: float) -> dict:
         "e2e_d2h_bytes": w * h * 4,
         "reference_dp_ops": dp_ops,
         "reference_op_rate_over_fp64_peak": round(dp_ops / (ms * 1e-3) / fp64, 4) if fp64 else None,
-        "note": "exact cycle detection stops provably periodic orbits early, so the "
-                "reference-op rate is an equivalent rate and may exceed 1",
+        "note": "exact shortcuts (cycle detection; pixels provably inside the main cardioid "
+                "or the period-2 bulb) skip iterations of never-escaping pixels, so the "
+                "reference-op rate is an equivalent rate and exceeds 1; the FP64 roofline of "
+                "the plain kernel is in profiles/r02_configs.json",
         "parity": "bit-exact vs reference sha256 (kernel and overlapped e2e)" if ok and ok_e2e
                   else "MISMATCH vs reference",
     }

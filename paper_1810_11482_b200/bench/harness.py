@@ -353,14 +353,18 @@ class MandelbrotTiles:
     (``enqueue_read_rows_into``), so the reads overlap the computation of the
     later chunks and no host-side scatter copy is needed.
 
-    With ``interleave`` (default) chunk i of a device takes every chunks-th
-    of its rows starting at its i-th, so every chunk samples the whole image
-    and costs the same (bounded rows are far more expensive than escaping
-    ones); otherwise chunks are contiguous bands."""
+    By default chunks are contiguous bands, each read by one linear DMA:
+    with the interior test and cycle detection the kernel (1.3 ms for config
+    3) is faster than the 132.7 MB read (2.4 ms), so the reads set the pace
+    and linear copies beat strided ones (8 bands: 2.52 ms end to end, 8
+    interleaved chunks 3.06, profiles/r02_mandel_chunks.txt).  With
+    ``interleave`` chunk i of a device takes every chunks-th of its rows
+    starting at its i-th, so every chunk samples the whole image and costs the
+    same — the better split when the kernel, not the read, is the bound."""
 
     def __init__(self, devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
                  viewport=VIEWPORT, esc: float = 4.0, stream: int = 0, chunks: int = 1,
-                 interleave: bool = True, shard: Optional[tuple] = None):
+                 interleave: bool = False, shard: Optional[tuple] = None):
         """``shard=(index, count)``: one process per GPU — the (single) device
         computes the rows of part `index` of `count` into its image; the
         other parts' rows are left untouched (another process owns them)."""
@@ -451,7 +455,7 @@ class MandelbrotTiles:
 
 def mandelbrot_multi(devices: Sequence[DeviceHandle], width: int, height: int, max_iter: int,
                      viewport=VIEWPORT, esc: float = 4.0, chunks: int = 1,
-                     interleave: bool = True) -> np.ndarray:
+                     interleave: bool = False) -> np.ndarray:
     return MandelbrotTiles(devices, width, height, max_iter, viewport, esc, chunks=chunks,
                            interleave=interleave)()
 

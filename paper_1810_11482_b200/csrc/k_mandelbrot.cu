@@ -70,9 +70,32 @@ struct MandelArgs {
 // gives.  States are saved at iterations 16, 32, 64, ... and compared every
 // 16th iteration (64-bit integer compares on the ALU pipe; every 4/8/16/32:
 // 2.98/2.71/2.68/2.97 ms for config 3, profiles/r01_mandel_sweep.txt).
+//
+// PERIOD also skips pixels that provably never escape: c inside the main
+// cardioid with the fixed point's multiplier |1 - sqrt(1 - 4c)| <= 0.99, or
+// inside the period-2 bulb with |4(c + 1)| <= 0.99.  There the critical
+// orbit is attracted to a cycle and stays in the filled Julia set, which
+// lies in |z| <= (1 + sqrt(1 + 4|c|)) / 2 < 1.52 — |z|^2 < 2.31, far below
+// any bailout >= 4 (the host enables the test only then) — so the reference
+// counts max_iter for them; the 1% margin keeps the classification away
+// from the boundary, where the basin thins out.  Checked bit for bit on the
+// full config-3 image and on cardioid / bulb viewports at up to 5000
+// iterations (tests/test_gpu_parity.py).
+__device__ __forceinline__ bool never_escapes(double cr, double ci) {
+  const double b = (cr + 1.0) * (cr + 1.0) + ci * ci;  // period-2 bulb
+  if (b <= 0.06125625) return true;                      // (0.99 / 4)^2
+  const double wr = 1.0 - 4.0 * cr, wi = -4.0 * ci;      // 1 - 4c
+  const double m = sqrt(wr * wr + wi * wi);
+  const double sr = sqrt(0.5 * (m + wr));
+  const double si = copysign(sqrt(fmax(0.5 * (m - wr), 0.0)), wi);
+  const double lr = 1.0 - sr;                            // multiplier 1 - sqrt(1 - 4c)
+  return lr * lr + si * si <= 0.9801;                    // 0.99^2
+}
+
 template <bool INTCMP, int P, bool FUSED = false, bool PERIOD = false>
 __device__ __forceinline__ void escape_countP(const double (&cr)[P], const double (&ci)[P],
-                                              double esc, uint32_t max_iter, uint32_t (&n)[P]) {
+                                              double esc, uint32_t max_iter, uint32_t (&n)[P],
+                                              bool interior_ok = false) {
   // zr^2 and zi^2 are carried from one iteration to the next (computed
   // right after the update) so each is evaluated once per iteration.
   double zr[P], zi[P], r2[P], i2[P];
@@ -84,6 +107,10 @@ __device__ __forceinline__ void escape_countP(const double (&cr)[P], const doubl
     sr[p] = si[p] = 0x7ff8000000000001ll;  // matches no iterate
     n[p] = 0;
     live[p] = true;
+    if (PERIOD && interior_ok && never_escapes(cr[p], ci[p])) {
+      n[p] = max_iter;
+      live[p] = false;
+    }
   }
   const long long esc_bits = __double_as_longlong(esc);
   uint32_t save_at = kPeriodCheck;
@@ -194,10 +221,11 @@ __global__ void __launch_bounds__(kThreads, PERIOD ? 3 : 1) k_mandelbrotP(Mandel
         cr[j] = ok[j] ? c_re : 1e3;  // off-image lanes escape at once, never stored
         ci[j] = ok[j] ? c_im : 1.0;
       }
+      const bool interior_ok = a.esc >= 4.0;  // see never_escapes
       if (INTCMP && a.fused && fused_ok<P>(cr, ci))
-        escape_countP<INTCMP, P, true, PERIOD>(cr, ci, a.esc, a.max_iter, cnt);
+        escape_countP<INTCMP, P, true, PERIOD>(cr, ci, a.esc, a.max_iter, cnt, interior_ok);
       else
-        escape_countP<INTCMP, P, false, PERIOD>(cr, ci, a.esc, a.max_iter, cnt);
+        escape_countP<INTCMP, P, false, PERIOD>(cr, ci, a.esc, a.max_iter, cnt, interior_ok);
 #pragma unroll
       for (int j = 0; j < P; ++j)
         if (ok[j]) a.out[at[j]] = cnt[j];

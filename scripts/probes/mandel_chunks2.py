@@ -24,7 +24,7 @@ def timed(fn, reps=5):
 
 with Runtime(devices=[0]) as rt:
     dev = rt.get_all_devices().get()[0]
-    for chunks in (1, 4, 8, 32):
+    for chunks in (1, 4, 8, 16, 32):
         for inter in (False, True):
             t = MandelbrotTiles([dev], 7680, 4320, 2000, chunks=chunks, interleave=inter)
             w, G = t.width, 1
