@@ -31,6 +31,7 @@ namespace {
 constexpr size_t kSlotBytes = 8u << 20;  // 8 MiB per staging slot
 constexpr int kSlots = 8;                // 64 MiB of pinned write staging per process
 constexpr size_t kPart = 1u << 20;       // copy task granularity
+constexpr size_t kHugePage = 2u << 20;   // reads into fresh memory: one task per huge page
 constexpr int kLag = 3;                  // chunks being copied ahead of the DMA issue
 
 // A fixed pool of copy threads taking independent memcpy tasks; a Group
@@ -63,17 +64,26 @@ class CopyPool {
  public:
   CopyPool() {
     const unsigned hw = std::thread::hardware_concurrency();
-    const int n = (int)std::max(2u, std::min(12u, hw ? hw - 1 : 4u));
+    const int n = (int)std::max(2u, std::min(15u, hw ? hw - 1 : 4u));
     for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
-  // split [src, src+n) -> dst into kPart tasks counted by g
-  void submit(void* dst, const void* src, size_t n, Group* g) {
-    const size_t parts = (n + kPart - 1) / kPart;
-    g->left.fetch_add((int)parts, std::memory_order_acq_rel);
+  // split [src, src+n) -> dst into tasks of `part` bytes counted by g; the
+  // cuts fall on multiples of `part` in the DESTINATION's address space, so
+  // no two threads first-touch the same (2 MiB huge) page of a fresh buffer
+  void submit(void* dst, const void* src, size_t n, Group* g, size_t part = kPart) {
+    std::vector<Task> tasks;
+    size_t off = 0;
+    while (off < n) {
+      const uintptr_t d = (uintptr_t)dst + off;
+      const size_t to_cut = part - (size_t)(d % part);
+      const size_t len = std::min(to_cut, n - off);
+      tasks.push_back(Task{(char*)dst + off, (const char*)src + off, len, g});
+      off += len;
+    }
+    g->left.fetch_add((int)tasks.size(), std::memory_order_acq_rel);
     {
       std::lock_guard<std::mutex> lk(mu_);
-      for (size_t off = 0; off < n; off += kPart)
-        q_.push_back(Task{(char*)dst + off, (const char*)src + off, std::min(kPart, n - off), g});
+      for (auto& t : tasks) q_.push_back(t);
     }
     cv_.notify_all();
   }
@@ -267,7 +277,7 @@ extern "C" int ofl_collect(ofl_read* r, void* dst) {
     }
     const uint64_t off = i * r->chunk;
     pool().submit((char*)dst + off, r->staging + off, (size_t)std::min(r->chunk, r->bytes - off),
-                  &g);
+                  &g, kHugePage);
   }
   pool().help(&g);
   g.wait();
