@@ -45,10 +45,12 @@ class Binding:
     launch: Callable
     # first out-of-bounds index (or None) given values and items
     oob: Optional[Callable] = None
-    # quick(stream_ptr, values, items) -> ticket > 0, 0 = take launch()
-    # (anything unusual, e.g. an out-of-bounds access), or -status: the
-    # handles' run fast path for the per-future-overhead-critical kernels
-    quick: Optional[Callable] = None
+    # plan(values, items) -> (fn, args) with fn(stream_ptr, *args) -> ticket
+    # | -status, or None (anything unusual, e.g. an out-of-bounds access:
+    # launch() reports it): the handles' run fast path for the
+    # per-future-overhead-critical kernels, cacheable while the registry
+    # generation holds
+    plan: Optional[Callable] = None
     # per parameter: 0 buffer, 1 scalar_f64, 2 scalar_u32 (the run fast path)
     codes: tuple = field(default=(), init=False, compare=False)
 
@@ -102,21 +104,21 @@ def _stream_binding(name: str, op: int, kinds: tuple) -> Binding:
             n if n < items else items, ticket,
         )
 
-    quick = None
+    plan = None
     if fast is not None:
         stream_op = fast.stream_op
 
-        def quick(sp, v, items):
+        def plan(v, items):
             a, b = v[0], v[1]
             c = v[2] if has_c else b
             n = v[-1]
             m = n if n < items else items
             if m > (a.size_bytes >> 3) or m > (b.size_bytes >> 3) or m > (c.size_bytes >> 3):
-                return 0  # launch() reports the out-of-bounds index
+                return None  # launch() reports the out-of-bounds index
             s = v[3] if op == _native.STREAM_TRIAD else (v[2] if has_s else 0.0)
-            return stream_op(sp, op, a.ptr, b.ptr, c.ptr, s, m)
+            return stream_op, (op, a.ptr, b.ptr, c.ptr, s, m)
 
-    return Binding(name, kinds, launch, oob, quick)
+    return Binding(name, kinds, launch, oob, plan)
 
 
 # -- stencil ---------------------------------------------------------------------
