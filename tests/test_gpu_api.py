@@ -20,6 +20,7 @@ from paper_1810_11482_b200 import (
     NotBuiltError,
     OobAccessError,
     Runtime,
+    UnknownGidError,
     copy,
     pinned_empty,
     when_all,
@@ -532,3 +533,35 @@ def test_when_all_runs_read_landing(dev):
     while not agg.done():
         assert time.time() - t0 < 30
     assert out3.tobytes() == payload.tobytes()
+
+
+def test_launch_and_write_plans_track_arguments(rt, dev):
+    """The handles' launch / pinned-write plans (handles.py) reuse a resolved
+    call only for the same argument objects: a changed scalar, a new pinned
+    payload, another stream or an unregistered buffer take the full path."""
+    n = 4096
+    prog = dev.create_program_with_source(kernel_source("stream")).get()
+    prog.build("triad").get()
+    A, B, C = (dev.create_buffer(n * 8).get() for _ in range(3))
+    b = pinned_empty(n * 8, np.float64)
+    c = pinned_empty(n * 8, np.float64)
+    b[:] = np.arange(n)
+    c[:] = 1.0
+    B.enqueue_write(0, b)
+    C.enqueue_write(0, c)
+    args = [A, B, C, 3.0, n]
+    grid, block = (n // 256, 1, 1), (256, 1, 1)
+    for s in (3.0, 3.0, 5.0, 5.0, 0.5):
+        args[3] = s
+        prog.run(args, "triad", grid, block)
+        got = np.frombuffer(A.enqueue_read(0, n * 8).get(), np.float64)
+        assert np.array_equal(got, np.arange(n) + s), s
+    s1 = dev.create_stream()
+    c[:] = 2.0
+    C.enqueue_write(0, c)  # same array again, new contents
+    prog.run(args, "triad", grid, block, s1).get()
+    got = np.frombuffer(A.enqueue_read(0, n * 8).get(), np.float64)
+    assert np.array_equal(got, np.arange(n) + 0.5 * 2.0)
+    rt.registry.unregister(C.gid)
+    with pytest.raises(UnknownGidError):
+        prog.run(args, "triad", grid, block).get()

@@ -150,6 +150,33 @@ SCRIPT = textwrap.dedent(
         dropped = huge.enqueue_read(0, pl.size)
         del dropped
         d0.synchronize().get()
+        # launch plans / pinned-write plans: reused only for the same objects
+        # under an unchanged registry generation
+        from paper_1810_11482_b200 import pinned_empty
+        tp = d0.create_program_with_source(kernel_source("stream")).get()
+        tp.build("triad").get()
+        TA, TB, TC = (d0.create_buffer(8 * 64).get() for _ in range(3))
+        targs = [TA, TB, TC, 3.0, 64]
+        g, blk = (1, 1, 1), (64, 1, 1)
+        for _ in range(3):
+            tp.run(targs, "triad", g, blk).get()
+        assert tp._qc is not None and tp._qc[3][0] is TA
+        targs[3] = 5.0                                  # a changed element: full path again
+        tp.run(targs, "triad", g, blk).get()
+        assert tp._qc[3][3] == 5.0
+        pin = pinned_empty(64)
+        pin[:] = 1
+        TB.enqueue_write(0, pin).get()
+        assert TB._wq is not None
+        pin[:] = 7                                      # same array, new contents: re-sent
+        TB.enqueue_write(0, pin).get()
+        assert TB.enqueue_read(0, 64).get() == bytes([7]) * 64
+        TB.enqueue_write(64, pin).get()                 # other offset: full path
+        assert TB.enqueue_read(64, 64).get() == bytes([7]) * 64
+        rt.registry.unregister(TC.gid)                  # generation moves: plans invalid
+        raises(UnknownGidError, lambda: tp.run(targs, "triad", g, blk).get())
+        rt.registry.unregister(TB.gid)
+        raises(UnknownGidError, lambda: TB.enqueue_write(0, pin).get())
         bad3 = DeviceToken(st, tk, boom)
         assert when_all([when_all([bad3])]).is_failed()
 
