@@ -235,13 +235,18 @@ def read_frame(sock: socket.socket) -> tuple:
 
 
 def send_frame(sock: socket.socket, lock: threading.Lock, opcode: int, request_id: int, gid,
-               payload=b"") -> None:
-    head = header(opcode, request_id, gid, len(payload))
+               payload=b"", tail=None) -> None:
+    """One frame: header, payload and an optional `tail` buffer appended to
+    the payload without joining them (a WRITE's data is sent in place)."""
+    tail_n = memoryview(tail).nbytes if tail is not None else 0
+    head = header(opcode, request_id, gid, len(payload) + tail_n)
     with lock:
-        if len(payload) < (64 << 10):
-            sock.sendall(head + bytes(payload))
+        if len(payload) + tail_n < (64 << 10):
+            sock.sendall(head + bytes(payload) + (bytes(tail) if tail_n else b""))
             return
         parts = [memoryview(head), memoryview(payload).cast("B")]
+        if tail_n:
+            parts.append(memoryview(tail).cast("B"))
         while parts:  # sendmsg may send part of the gathered buffers
             sent = sock.sendmsg(parts)
             while sent and parts:
@@ -422,7 +427,7 @@ class RemoteLocality:
                                         daemon=True)
         self._reader.start()
 
-    def _request(self, op: int, gid, payload=b"") -> CompletionToken:
+    def _request(self, op: int, gid, payload=b"", tail=None) -> CompletionToken:
         promise = Promise()
         if self._dead is not None:
             return make_failed(TransportLostError(f"connection to {self.address} lost"))
@@ -430,7 +435,7 @@ class RemoteLocality:
         with self._pending_lock:
             self._pending[rid] = promise
         try:
-            send_frame(self._sock, self._send_lock, op, rid, gid, payload)
+            send_frame(self._sock, self._send_lock, op, rid, gid, payload, tail)
         except OSError as exc:
             self._fail_all(exc)
         if self._dead is not None:  # the reader may have drained _pending first
@@ -501,10 +506,12 @@ class RemoteLocality:
         return self._request(Opcode.CREATE_BUFFER, device_gid, _U64.pack(size)).then(decode_gid)
 
     def write(self, buffer_gid, offset, data, stream, device=None) -> CompletionToken:
-        body = memoryview(data).cast("B") if not isinstance(data, bytes) else data
-        payload = _U64.pack(offset) + _U32.pack(stream) + bytes(body)
-        return self._track(device, stream,
-                           self._request(Opcode.WRITE, buffer_gid, payload).then(lambda _: None))
+        # the data goes out in place (sendmsg); the request is fully sent when
+        # this returns, so the caller may reuse it, as with any write
+        body = data if isinstance(data, bytes) else memoryview(data).cast("B")
+        prefix = _U64.pack(offset) + _U32.pack(stream)
+        return self._track(device, stream, self._request(Opcode.WRITE, buffer_gid, prefix,
+                                                         body).then(lambda _: None))
 
     def read(self, buffer_gid, offset, size, stream, device=None) -> CompletionToken:
         payload = struct.pack("<QQI", offset, size, stream)
