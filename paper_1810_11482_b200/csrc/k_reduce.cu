@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(kThreads) k_dot_f32(const float* __restrict__ 
 // CTA's fold over ~10^5 partials cost more than the tail it balances.  CTAs
 // per SM per kernel from the read-bandwidth sweep (scripts/probes/
 // read_bw_probe.cu, scripts/reduce_sweep.sh).
-int grid_for(ofl_stream* s, uint64_t vec_units, int unroll, int cps) {  uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
+int grid_for(ofl_stream* s, uint64_t vec_units, int unroll, int cps) {
+  uint64_t blocks = (vec_units + (uint64_t)kThreads * unroll - 1) / ((uint64_t)kThreads * unroll);
   uint64_t cap = (uint64_t)ofl::num_sms(s->dev) * cps;
   if (cap > kMaxBlocks) cap = kMaxBlocks;
   if (blocks > cap) blocks = cap;
