@@ -387,6 +387,16 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   if (e != cudaSuccess) return cuda_error(e, "memory pool setup");
   void* p = nullptr;
   e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
+  if (e == cudaErrorMemoryAllocation) {
+    // frees still queued behind other streams' work hold memory: let them
+    // complete, then retry once
+    (void)cudaGetLastError();
+    {
+      std::lock_guard<std::mutex> f(g_free_mu[dev]);
+      if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
+    }
+    e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
+  }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     if (e == cudaErrorMemoryAllocation) return oom(dev, bytes);
@@ -411,6 +421,19 @@ int ofl_malloc_shareable(int dev, uint64_t bytes, void** dptr) {
   if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
   void* p = nullptr;
   e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    // the stream-ordered pool keeps freed memory: hand it back and retry
+    (void)cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      {
+        std::lock_guard<std::mutex> f(g_free_mu[dev]);
+        if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
+      }
+      cudaMemPoolTrimTo(pool, 0);
+    }
+    e = cudaMalloc(&p, bytes);
+  }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     if (e == cudaErrorMemoryAllocation) return oom(dev, bytes);
