@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/ofl.h"
 
@@ -48,6 +49,10 @@ struct ofl_event {
 
 namespace ofl {
 
+constexpr int kMaxDev = 64;
+// device buffers of this size and up are VMM mappings (ofl_vmm.cu)
+constexpr size_t kVmmMin = 2u << 20;
+
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* what);
 cudaError_t use_device(int dev);
@@ -59,6 +64,13 @@ cudaError_t stream_launch(cudaStream_t st, int sms, int op, double* a, const dou
                           const double* c, double scalar, uint64_t n);
 // cudaDeviceEnablePeerAccess(from -> to) once per pair, if the pair supports it
 void enable_peer(int from, int to);
+// VMM allocations (ofl_vmm.cu)
+bool vmm_available();
+int vmm_alloc(int dev, size_t bytes, void** out);
+bool vmm_owns(void* p);
+bool vmm_free_after(void* p, std::vector<cudaEvent_t>& fences);
+void vmm_drain();
+void vmm_grant_peer(int from, int to);
 // Scratch of at least `bytes` on the stream's device (caller holds s->mu).
 int stream_scratch(ofl_stream* s, size_t bytes, void** out);
 

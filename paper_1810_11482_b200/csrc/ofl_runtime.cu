@@ -44,7 +44,6 @@ cudaError_t use_device(int dev) {
   return cudaSetDevice(dev);
 }
 
-static constexpr int kMaxDev = 64;
 static int g_sms[kMaxDev];
 
 int num_sms(int dev) {
@@ -177,7 +176,8 @@ static void CUDART_CB host_complete(void* p) {
 }
 
 // ------------------------------------------------------------- memory ---
-// Buffers come from each device's stream-ordered memory pool (cudaMallocAsync
+// Buffers of kVmmMin bytes and up are VMM mappings (ofl_vmm.cu); smaller
+// ones come from each device's stream-ordered memory pool (cudaMallocAsync
 // on a per-device internal stream; the pool keeps freed memory for reuse
 // instead of returning it to the driver).  A free is ordered on the device
 // after the work enqueued so far on every stream of the process — the
@@ -238,7 +238,9 @@ void enable_peer(int from, int to) {
     cudaSetDevice(from);
     cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
     if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
-    // stream-ordered allocations need an explicit grant per accessing device
+    // stream-ordered and VMM allocations need an explicit grant per
+    // accessing device
+    vmm_grant_peer(from, to);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, to) == cudaSuccess) {
       cudaMemAccessDesc d{};
@@ -385,7 +387,25 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   e = internal_stream(dev);
   if (e == cudaSuccess) e = pool_setup(dev);
   if (e != cudaSuccess) return cuda_error(e, "memory pool setup");
+  // a request beyond the device's capacity fails at once
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && bytes > total_b) return oom(dev, bytes);
   void* p = nullptr;
+  if (bytes >= kVmmMin && vmm_available()) {
+    // large buffers: their own mapping (fast to create, freed without any
+    // device-wide synchronisation; ofl_vmm.cu)
+    const int st = vmm_alloc(dev, bytes, &p);
+    if (st) return st;
+    e = cudaMemsetAsync(p, 0, bytes, g_zero_stream[dev]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_zero_stream[dev]);
+    if (e != cudaSuccess) {
+      std::vector<cudaEvent_t> none;
+      vmm_free_after(p, none);
+      return cuda_error(e, "zero fill");
+    }
+    *dptr = p;
+    return OFL_OK;
+  }
   e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
   if (e == cudaErrorMemoryAllocation) {
     // frees still queued behind other streams' work hold memory: let them
@@ -470,6 +490,27 @@ int ofl_free(int dev, void* dptr) {
     // drain before they are released (registry.py:104-109 semantics)
     e = cudaFree(dptr);
     if (e != cudaSuccess) return cuda_error(e, "cudaFree");
+    return OFL_OK;
+  }
+  if (vmm_owns(dptr)) {
+    // released by the reaper once a fence recorded now on every live stream
+    // (of any device: peer copies, peer stores) has passed
+    std::vector<cudaEvent_t> fences;
+    {
+      std::lock_guard<std::mutex> l(g_streams_mu);
+      for (ofl_stream* s : g_streams) {
+        if (use_device(s->dev) != cudaSuccess) continue;
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) continue;
+        if (cudaEventRecord(ev, s->cs) == cudaSuccess)
+          fences.push_back(ev);
+        else
+          cudaEventDestroy(ev);
+      }
+    }
+    (void)cudaGetLastError();
+    use_device(dev);
+    vmm_free_after(dptr, fences);
     return OFL_OK;
   }
   // ordered after the work enqueued so far on every live stream (any device
