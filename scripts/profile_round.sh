@@ -15,6 +15,6 @@ $N -k regex:k_stencil2d -s 2 -c 1 -o gpurun_out/${P}_stencil2d python scripts/be
 $N -k regex:k_heat_pipe -s 2 -c 1 -o gpurun_out/${P}_heat python scripts/profile_kernels.py heat 1 > gpurun_out/ncu_heat.log 2>&1
 $N -k regex:k_dot -s 1 -c 1 -o gpurun_out/${P}_dot python scripts/profile_kernels.py dot > gpurun_out/ncu_dot.log 2>&1
 $N -k regex:k_sum -s 1 -c 1 -o gpurun_out/${P}_sum python scripts/profile_kernels.py sum > gpurun_out/ncu_sum.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/${P}_bench_launches.csv python bench.py --steps 200 --warmup 5 --no-overhead --cpu-seconds 0 --e2e-steps 2 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/${P}_bench_launches.csv python bench.py --steps 200 --warmup 5 --configs "" --no-overhead --cpu-seconds 0 --e2e-steps 2 > /dev/null 2>&1
 bash scripts/sanitize.sh > gpurun_out/sanitizer.txt 2>&1
 ls gpurun_out
