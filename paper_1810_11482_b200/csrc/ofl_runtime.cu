@@ -378,6 +378,21 @@ static int oom(int dev, uint64_t bytes) {
                                     " bytes requested, allocation failed");
 }
 
+// hand every byte freed memory holds back to the device (before retrying an
+// allocation that ran out): frees still queued behind other streams' work,
+// the stream-ordered pool's kept blocks, released VMM mappings
+static void reclaim(int dev) {
+  {
+    std::lock_guard<std::mutex> f(g_free_mu[dev]);
+    if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  vmm_drain();
+  vmm_trim(dev);
+  (void)cudaGetLastError();
+}
+
 int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   if (bytes == 0) return set_error(OFL_ERR_BAD_ARGS, "buffer size must be positive");
   if (dev < 0 || dev >= kMaxDev) return set_error(OFL_ERR_BAD_ARGS, "bad device ordinal");
@@ -394,7 +409,11 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   if (bytes >= kVmmMin && vmm_available()) {
     // large buffers: their own mapping (fast to create, freed without any
     // device-wide synchronisation; ofl_vmm.cu)
-    const int st = vmm_alloc(dev, bytes, &p);
+    int st = vmm_alloc(dev, bytes, &p);
+    if (st == OFL_ERR_OOM) {
+      reclaim(dev);
+      st = vmm_alloc(dev, bytes, &p);
+    }
     if (st) return st;
     e = cudaMemsetAsync(p, 0, bytes, g_zero_stream[dev]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(g_zero_stream[dev]);
@@ -408,13 +427,8 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
   }
   e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
   if (e == cudaErrorMemoryAllocation) {
-    // frees still queued behind other streams' work hold memory: let them
-    // complete, then retry once
     (void)cudaGetLastError();
-    {
-      std::lock_guard<std::mutex> f(g_free_mu[dev]);
-      if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
-    }
+    reclaim(dev);
     e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
   }
   if (e != cudaSuccess) {
@@ -442,16 +456,8 @@ int ofl_malloc_shareable(int dev, uint64_t bytes, void** dptr) {
   void* p = nullptr;
   e = cudaMalloc(&p, bytes);
   if (e == cudaErrorMemoryAllocation) {
-    // the stream-ordered pool keeps freed memory: hand it back and retry
     (void)cudaGetLastError();
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      {
-        std::lock_guard<std::mutex> f(g_free_mu[dev]);
-        if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
-      }
-      cudaMemPoolTrimTo(pool, 0);
-    }
+    reclaim(dev);
     e = cudaMalloc(&p, bytes);
   }
   if (e != cudaSuccess) {

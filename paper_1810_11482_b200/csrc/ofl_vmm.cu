@@ -9,9 +9,11 @@
 // get their own physical allocation (cuMemCreate + cuMemAddressReserve +
 // cuMemMap + cuMemSetAccess: ~2 ms per GiB), and their free is deferred:
 // ofl_free records a fence event on every live stream and hands the mapping
-// to a reaper thread, which waits for those events and only then unmaps —
-// cuMemUnmap / cuMemRelease do not synchronise with other streams (same
-// probe), so no stream ever stalls on a dropped buffer.
+// to a reaper thread, which waits for those events and then caches it for
+// reuse by an allocation of the same size (unmapped — cuMemUnmap does not
+// synchronise with other streams, same probe — only when an allocation runs
+// out of memory), so no stream ever stalls on a dropped buffer and
+// steady-state allocations make no driver call.
 //
 // Driver entry points come from cudaGetDriverEntryPoint (libofl.so does not
 // link libcuda; the runtime resolves the driver it already loaded).
@@ -19,6 +21,7 @@
 
 #include <condition_variable>
 #include <deque>
+#include <map>
 #include <set>
 #include <thread>
 #include <unordered_map>
@@ -83,8 +86,12 @@ struct Mapping {
   size_t size;
 };
 
-std::mutex g_mu;                              // mappings + peer grants
+std::mutex g_mu;                              // mappings, cache, peer grants
 std::unordered_map<uintptr_t, Mapping> g_live;
+// released mappings whose fences have passed, by size: reused as they are
+// (a fresh physical allocation can wait behind queued work, a cached one
+// never does); unmapped only when an allocation runs out of memory
+std::multimap<size_t, Mapping> g_cache[ofl::kMaxDev];
 std::set<int> g_peers[ofl::kMaxDev];          // devices granted access to dev's buffers
 
 // deferred frees: a mapping and the fence events it must outlive
@@ -128,7 +135,10 @@ void reaper() {
       cudaEventDestroy(e);
     }
     (void)cudaGetLastError();
-    unmap(p.m);
+    {
+      std::lock_guard<std::mutex> g(g_mu);
+      g_cache[p.m.dev].emplace(p.m.size, p.m);
+    }
     {
       std::lock_guard<std::mutex> lk(Q.mu);
       --Q.busy;
@@ -166,13 +176,20 @@ int vmm_alloc(int dev, size_t bytes, void** out) {
   if (d.gran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || !gran)
     gran = 2u << 20;
   const size_t size = (bytes + gran - 1) / gran * gran;
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_cache[dev].find(size);
+    if (it != g_cache[dev].end()) {  // a released mapping of this size
+      const Mapping m = it->second;
+      g_cache[dev].erase(it);
+      g_live[(uintptr_t)m.va] = m;
+      *out = reinterpret_cast<void*>(m.va);
+      return OFL_OK;
+    }
+  }
   CUmemGenericAllocationHandle h;
   CUresult r = d.create(&h, size, &prop, 0);
-  if (r == CUDA_ERROR_OUT_OF_MEMORY) {
-    vmm_drain();  // pending frees may hold enough memory
-    r = d.create(&h, size, &prop, 0);
-  }
-  if (r == CUDA_ERROR_OUT_OF_MEMORY)
+  if (r == CUDA_ERROR_OUT_OF_MEMORY)  // the caller reclaims freed memory and retries
     return set_error(OFL_ERR_OOM, "cuda" + std::to_string(dev) + ": " + std::to_string(bytes) +
                                       " bytes requested, allocation failed");
   if (r != CUDA_SUCCESS) return set_error(OFL_ERR_CUDA, "cuMemCreate failed: " + std::to_string(r));
@@ -239,6 +256,16 @@ void vmm_drain() {
   Q.idle_cv.wait(lk, [&] { return Q.q.empty() && Q.busy == 0; });
 }
 
+// unmap every cached mapping of `dev` (before retrying a failed allocation)
+void vmm_trim(int dev) {
+  std::multimap<size_t, Mapping> drop;
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    drop.swap(g_cache[dev]);
+  }
+  for (auto& kv : drop) unmap(kv.second);
+}
+
 // `from` may now read and write `to`'s VMM buffers, current and future
 void vmm_grant_peer(int from, int to) {
   const Driver& d = driver();
@@ -251,6 +278,7 @@ void vmm_grant_peer(int from, int to) {
   a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
   for (auto& kv : g_live)
     if (kv.second.dev == to) d.access(kv.second.va, kv.second.size, &a, 1);
+  for (auto& kv : g_cache[to]) d.access(kv.second.va, kv.second.size, &a, 1);
 }
 
 }  // namespace ofl

@@ -15,11 +15,16 @@ pytestmark = pytest.mark.gpu
 
 def _warm(rt, dev):
     """First use of each allocation path (driver entry points, the reaper
-    thread, pool setup) outside the measured part."""
-    for size in (4 << 20, 1 << 10):
+    thread, pool setup) outside the measured part, and one released buffer
+    of each size the tests allocate: a first-time physical allocation may
+    wait behind queued work inside the driver; steady-state allocations
+    reuse released memory and make no driver call."""
+    for size in (32 << 20, 4 << 20, 4 << 20, 1 << 20, 1 << 10):
         b = dev.create_buffer(size).get()
         rt.registry.unregister(b.gid)
         del b
+    dev.synchronize().get()
+    time.sleep(0.05)  # the reaper has passed their (already complete) fences
 
 
 def _long_heat(dev, stream: int, n: int = 1 << 27, steps: int = 3000):
@@ -85,3 +90,28 @@ def test_allocation_after_free_does_not_wait(rt, dev):
     assert fresh.enqueue_read(0, 16).get() == bytes(16)
     tok.get()
     assert dt < 0.05, dt
+
+
+def test_released_memory_is_reclaimed_for_other_sizes(rt, dev):
+    """Released VMM mappings are kept for reuse by same-size allocations;
+    an allocation of another size that does not fit otherwise gets them
+    back (ofl_runtime.cu reclaim: pool trim + cached mappings unmapped)."""
+    import torch
+
+    free0, total = torch.cuda.mem_get_info(0)
+    piece = 8 << 30
+    count = int(free0 * 0.7) // piece
+    held = [dev.create_buffer(piece).get() for _ in range(count)]
+    for b in held:
+        rt.registry.unregister(b.gid)
+    del held, b
+    dev.synchronize().get()
+    time.sleep(0.2)
+    # larger than what is free unless the released mappings are unmapped
+    big = int(free0 * 0.8)
+    b = dev.create_buffer(big).get()
+    assert b.enqueue_read(big - 16, 16).get() == bytes(16)
+    rt.registry.unregister(b.gid)
+    del b
+    small = dev.create_buffer(1 << 10).get()
+    assert small.enqueue_read(0, 16).get() == bytes(16)
