@@ -197,10 +197,16 @@ static std::set<ofl_stream*> g_streams;
 static std::mutex g_legacy_mu;                  // cudaMalloc'd (shareable) buffers
 static std::unordered_set<void*> g_legacy;
 
-// the internal stream of `dev` (created on first use; caller holds g_zero_mu[dev])
+// the internal stream of `dev` (created on first use; caller holds
+// g_zero_mu[dev]), at the device's highest priority: a zero fill is a short
+// kernel that must not queue behind the pending CTAs of a long kernel chain
+// on another stream (it gets the SMs at the chain's next kernel boundary)
 static cudaError_t internal_stream(int dev) {
   if (g_zero_stream[dev]) return cudaSuccess;
-  return cudaStreamCreateWithFlags(&g_zero_stream[dev], cudaStreamNonBlocking);
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e != cudaSuccess) return e;
+  return cudaStreamCreateWithPriority(&g_zero_stream[dev], cudaStreamNonBlocking, greatest);
 }
 
 static cudaError_t pool_setup(int dev) {
