@@ -758,8 +758,7 @@ def multi_mandelbrot(rt, dev, lib, D, rank: int, world: int) -> dict:
     }
 
 
-def run_multi_configs(rt, dev, lib, D, rank: int, world: int, names) -> dict:
-    out = {}
+def run_multi_configs(rt, dev, lib, D, rank: int, world: int, names, out: dict) -> dict:
     for name in names:
         t0 = time.time()
         fn = {"heat": multi_heat, "dot": multi_dot, "mandelbrot": multi_mandelbrot}[name]
@@ -772,8 +771,7 @@ def run_multi_configs(rt, dev, lib, D, rank: int, world: int, names) -> dict:
     return out
 
 
-def run_configs(rt, dev, lib, names) -> dict:
-    out = {}
+def run_configs(rt, dev, lib, names, out: dict) -> dict:
     st = rt.device_objects()[0].stream(0)
     fp64 = fp64_peak_ops(lib, st)
     for name in names:
@@ -906,16 +904,6 @@ def run_ours(args) -> None:
         ks = tuple(int(k) for k in args.overhead_ks.split(",") if k)
         overhead = OverheadBench(dev, rt).sweep(ks)
 
-    configs = None
-    names = [c for c in args.configs.split(",") if c]
-    if rank == 0 and world == 1 and names:
-        configs = run_configs(rt, dev, lib, names)
-        configs["overhead"] = overhead
-    elif world > 1 and names and (not oversubscribed or args.force_multi):
-        # configs 2-4 across the ranks (every rank takes part; rank 0 reports)
-        configs = run_multi_configs(rt, dev, lib, dist, rank, world, names)
-        configs["overhead"] = overhead
-
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
         r = cpu_triad_rate(n, args.cpu_seconds, 1)
@@ -927,53 +915,85 @@ def run_ours(args) -> None:
         }
 
     traffic = ncu_traffic().get("triad")
-    if rank == 0:
-        line = {
-            "metric": METRIC,
-            "value": round(value, 3),
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(job_ms / args.steps, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(n, world),
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 2),
+            "peak": peak,
             "unit": "GB/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": round(job_ms / args.steps, 5),
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic",
-            "config": workload_config(n, world),
-            "roofline": {
-                "bound": "hbm",
-                "achieved": round(achieved, 2),
-                "peak": peak,
-                "unit": "GB/s",
-                "frac": round(achieved / peak, 4),
-                "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
-                "traffic": traffic,
-                "peak_source": peak_src,
-                "kernel": "k_stream_tile<TRIAD,512,1,PDL> (csrc/k_stream.cu; programmatic dependent launch)",
-                "algorithmic_bytes_per_launch": step_bytes,
-                "avg_launch_us": round(avg_launch_ms * 1e3, 3),
-            },
-            "e2e": {
-                "value": round(e2e_value, 3),
-                "unit": "GB/s",
-                "h2d_bytes_per_step": 2 * n * 8,
-                "d2h_bytes_per_step": n * 8,
-                "steps": args.e2e_steps,
-                "ms_per_step": round(e2e_s / args.e2e_steps * 1e3, 3),
-                "schedule": "write b, write c (pinned), run, read_into a (pinned) per step; "
-                f"steps rotate over {nsets} streams x {nsets} device buffer sets; wall clock",
-            },
-            "cpu_baseline": cpu,
-            "gpu_launches": int(launches),
-            "clocks": clocks,
-            "clocks_per_rank": clocks_per_rank if world > 1 else None,
-            "future_overhead_us": overhead,
-            "configs": configs,
-            "parity": "bit-exact vs CPU oracle (oracle/ofl_oracle.c)",
-            "oversubscribed": oversubscribed,
-        }
+            "frac": round(achieved / peak, 4),
+            "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
+            "traffic": traffic,
+            "peak_source": peak_src,
+            "kernel": "k_stream_tile<TRIAD,512,1,PDL> (csrc/k_stream.cu; programmatic dependent launch)",
+            "algorithmic_bytes_per_launch": step_bytes,
+            "avg_launch_us": round(avg_launch_ms * 1e3, 3),
+        },
+        "e2e": {
+            "value": round(e2e_value, 3),
+            "unit": "GB/s",
+            "h2d_bytes_per_step": 2 * n * 8,
+            "d2h_bytes_per_step": n * 8,
+            "steps": args.e2e_steps,
+            "ms_per_step": round(e2e_s / args.e2e_steps * 1e3, 3),
+            "schedule": "write b, write c (pinned), run, read_into a (pinned) per step; "
+            f"steps rotate over {nsets} streams x {nsets} device buffer sets; wall clock",
+        },
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "clocks_per_rank": clocks_per_rank if world > 1 else None,
+        "future_overhead_us": overhead,
+        "configs": None,
+        "parity": "bit-exact vs CPU oracle (oracle/ofl_oracle.c)",
+        "oversubscribed": oversubscribed,
+    }
+
+    # configs 2-4 after the headline.  A watchdog bounds them: if they have
+    # not finished within --configs-budget seconds (a hung peer exchange on
+    # some rank, say), every rank leaves and rank 0 still prints the headline
+    # with the configs that did finish.
+    names = [c for c in args.configs.split(",") if c]
+    multi = world > 1 and names and (not oversubscribed or args.force_multi)
+    if (rank == 0 and world == 1 and names) or multi:
+        configs: dict = {}
+        line["configs"] = configs
+        finished = threading.Event()
+
+        def watchdog() -> None:
+            if finished.wait(args.configs_budget):
+                return
+            if rank == 0:
+                for name in names:
+                    configs.setdefault(name, {"error": f"not finished within --configs-budget "
+                                                       f"{args.configs_budget:g} s"})
+                configs["overhead"] = overhead
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        if multi:
+            # configs 2-4 across the ranks (every rank takes part; rank 0 reports)
+            run_multi_configs(rt, dev, lib, dist, rank, world, names, configs)
+        else:
+            run_configs(rt, dev, lib, names, configs)
+        configs["overhead"] = overhead
+        finished.set()
+
+    if rank == 0:
         print(json.dumps(line), flush=True)
     rt.close()
     dist.close()
@@ -1031,6 +1051,8 @@ def main(argv=None) -> None:
                     help="permit OFL_* run-changing switches (sweeps only, never a headline)")
     ap.add_argument("--configs", default="heat,mandelbrot,dot",
                     help="BASELINE configs 2-4 measured after the headline (N=1 only); '' = none")
+    ap.add_argument("--configs-budget", type=float, default=600.0,
+                    help="seconds the configs may take before the headline is printed without them")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="--impl reference: approximate length of the K timed steps")
