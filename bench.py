@@ -712,7 +712,7 @@ def multi_dot(rt, dev, lib, D, rank: int, world: int) -> dict:
     rel = abs(got - total) / abs(total)
     peak, _ = hbm_peak()
     gbs = 8.0 * n / (ms * 1e-3) / 1e9
-    return {
+    out = {
         "workload": f"dot fp32 N=2^31 (BASELINE config 4) over {world} GPUs, one process each, "
                     "partials exchanged inside the reduction kernel over peer memory",
         "scaling": "strong", "n_gpus": world, "kernel_ms_max_over_ranks": round(ms, 4),
@@ -721,6 +721,41 @@ def multi_dot(rt, dev, lib, D, rank: int, world: int) -> dict:
         "parity": "within 1e-12 (tolerance 1e-5)" if rel <= 1e-12 else
                   ("within 1e-5" if rel <= 1e-5 else "MISMATCH"),
     }
+    # the same step with the library collective instead: the dot_f32 builtin
+    # into R, then one ncclAllReduce of the 8-byte partial on the same stream
+    try:
+        from paper_1810_11482_b200.collectives import Communicator
+
+        comm = Communicator.from_process_group(rt, dev)
+        prog = dev.create_builtin_program().get()
+        prog.build("dot_f32").get()
+        grid = (max(1, m // 256), 1, 1)
+
+        def step() -> None:
+            prog.run([A, B, R, m], "dot_f32", grid, (256, 1, 1))
+            comm.allreduce([R], count=1, dtype="f64")
+
+        for _ in range(3):
+            step()
+        dev.synchronize().get()
+        D.barrier()
+        t.start()
+        for _ in range(K):
+            step()
+        ms_nccl = D.max(t.stop() / K)
+        got = float(np.frombuffer(R.enqueue_read(0, 8).get(), np.float64)[0])
+        comm.close()
+        rel_nccl = abs(got - total) / abs(total)
+        out["nccl_allreduce"] = {
+            "kernel_ms_max_over_ranks": round(ms_nccl, 4),
+            "gbs_whole_job": round(8.0 * n / (ms_nccl * 1e-3) / 1e9, 1),
+            "rel_err_vs_oracle": rel_nccl,
+            "parity": "within 1e-12 (tolerance 1e-5)" if rel_nccl <= 1e-12 else
+                      ("within 1e-5" if rel_nccl <= 1e-5 else "MISMATCH"),
+        }
+    except Exception as exc:  # noqa: BLE001 - reported beside the fused result
+        out["nccl_allreduce"] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def multi_mandelbrot(rt, dev, lib, D, rank: int, world: int) -> dict:
