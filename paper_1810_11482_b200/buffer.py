@@ -13,7 +13,7 @@ import ctypes
 import threading
 
 from . import _native, hostmem
-from .completion import DeviceToken
+from .completion import DeviceToken, PipelinedToken
 from .device import DeviceObject
 from .errors import BadArgsError, OobAccessError
 from .futures import CompletionToken, make_ready
@@ -161,7 +161,6 @@ class BufferObject:
         st.keep(ticket.value, landing.release_later)
         return DeviceToken(st, ticket.value, lambda: (landing.take(), out)[1])
 
-
     def _read_chunked(self, st, offset: int, n: int, into) -> CompletionToken:
         """Large read to pageable memory: chunked D2H into a pinned staging
         block (one event per chunk); the token's finish step copies each
@@ -178,7 +177,7 @@ class BufferObject:
             raise_status(status, "read")
         landing = _ChunkedLanding(st.lib, block, n, handle.value, into)
         st.keep(ticket.value, landing.release_later)
-        return DeviceToken(st, ticket.value, landing.take)
+        return PipelinedToken(st, ticket.value, landing.take)
 
     def enqueue_read_rows_into(self, offset: int, out, row_bytes: int, rows: int,
                                dst_offset: int, dst_pitch: int, stream: int = 0):

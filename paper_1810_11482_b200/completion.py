@@ -222,4 +222,26 @@ class DeviceToken(CompletionToken):
             self._fail(status, "completion notify failed")
 
 
+class PipelinedToken(DeviceToken):
+    """Device token whose ``finish`` itself waits for the operation, piece by
+    piece: a chunked read (``ofl_collect`` waits for each chunk's event and
+    copies it out while the later chunks are still on the link).  ``get()``
+    starts the finish at once instead of first waiting for the whole
+    operation, so the host copies overlap the DMA; the finish fails the
+    token if the device faulted (the chunk events report it)."""
+
+    __slots__ = ()
+
+    def _block(self, timeout: Optional[float]) -> bool:
+        if self._state != _PENDING:
+            return True
+        if timeout is not None:
+            return DeviceToken._block(self, timeout)
+        self._finish_now()
+        if self._state == _PENDING:  # another thread is running finish()
+            self._wait_quiet(None)
+        return True
+
+
 DEVICE_TOKEN_TYPES.add(DeviceToken)
+DEVICE_TOKEN_TYPES.add(PipelinedToken)

@@ -16,6 +16,10 @@
 // step) waits for each chunk's event and hands it to the copy threads, so
 // the copy into the pageable destination of chunk k overlaps the DMA of the
 // chunks after it.
+#include <immintrin.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -59,6 +63,52 @@ struct Task {
   size_t n;
   Group* g;
 };
+
+// Copy with non-temporal (streaming) stores: the destination lines go to
+// DRAM without being read first (no read-for-ownership) and without
+// evicting the cache.  On the GPU box's host, 15 threads copy 256 MiB into
+// resident memory at 80 GB/s this way against 54 GB/s with memcpy
+// (profiles/r02_nt_copy.txt, scripts/probes/nt_copy_probe.c).
+__attribute__((target("avx2"))) void copy_stream(char* d, const char* s, size_t n) {
+  size_t head = (32 - ((uintptr_t)d & 31)) & 31;
+  if (head > n) head = n;
+  std::memcpy(d, s, head);
+  d += head, s += head, n -= head;
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 64));
+    const __m256i e = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 96), e);
+  }
+  std::memcpy(d + i, s + i, n - i);
+  _mm_sfence();  // the streamed lines are globally visible before the task counts as done
+}
+
+const bool g_avx2 = __builtin_cpu_supports("avx2");
+const uintptr_t g_page = (uintptr_t)sysconf(_SC_PAGESIZE);
+
+// One copy task.  Into resident memory (pinned staging slots, a caller's
+// array) streaming stores win; into fresh memory — a new bytes object,
+// first-touched by this very copy — the page fault dominates and plain
+// memcpy is slightly faster (44.7 vs 42.0 GB/s), so the task asks the kernel
+// whether its first destination page is resident (mincore: one syscall per
+// task of up to 2 MiB).
+void run_task(const Task& t) {
+  if (g_avx2 && t.n >= 4096) {
+    unsigned char resident = 0;
+    void* page = (void*)((uintptr_t)t.dst & ~(g_page - 1));
+    if (mincore(page, 1, &resident) == 0 && (resident & 1)) {
+      copy_stream(t.dst, t.src, t.n);
+      return;
+    }
+  }
+  std::memcpy(t.dst, t.src, t.n);
+}
 
 class CopyPool {
  public:
@@ -104,7 +154,7 @@ class CopyPool {
         t = q_.front();
         q_.pop_front();
       }
-      std::memcpy(t.dst, t.src, t.n);
+      run_task(t);
       t.g->done_one();
     }
   }
@@ -119,7 +169,7 @@ class CopyPool {
         t = q_.front();
         q_.pop_front();
       }
-      std::memcpy(t.dst, t.src, t.n);
+      run_task(t);
       t.g->done_one();
     }
   }
