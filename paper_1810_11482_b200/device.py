@@ -43,6 +43,22 @@ class DeviceInfo:
     def meets(self, major: int, minor: int) -> bool:
         return tuple(self.capability) >= (major, minor)
 
+    def _key(self) -> tuple:
+        return (self.name, tuple(self.capability), self.memory_bytes, self.compute_units)
+
+    # equal to any snapshot with the same fields — the reference's own
+    # DeviceInfo included (a daemon's view decoded by the reference's client
+    # equals this object, reference tests/test_transport.py:54-59)
+    def __eq__(self, other) -> bool:
+        try:
+            return self._key() == (other.name, tuple(other.capability), other.memory_bytes,
+                                   other.compute_units)
+        except (AttributeError, TypeError):
+            return NotImplemented
+
+    def __hash__(self) -> int:
+        return hash(self._key())
+
 
 @dataclass(frozen=True)
 class PhysicalInfo:

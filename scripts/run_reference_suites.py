@@ -11,8 +11,11 @@ as-is) and redefines those four: the runtime is an unmodified
 attached (``offloadrt_backend.attach``), and the device is the B200 as a
 reference ``DeviceHandle`` — so ``create_buffer``, ``enqueue_write/read``,
 ``build``, ``run``, ``when_all`` and ``copy`` in those tests execute through
-the reference's handles on the CUDA dispatch.  Tests that construct their
-own ``Runtime(backend=...)`` still exercise the reference itself.
+the reference's handles on the CUDA dispatch.  ``loopback`` /
+``host_loopback`` (a reference client connected to a daemon) get this
+package's daemon serving the B200 over the parcel protocol instead of the
+reference's sim / host daemon.  Tests that construct their own
+``Runtime(backend=...)`` still exercise the reference itself.
 
 The reference tests and package are read from ``--tests`` / ``--src``
 (defaults: /root/reference/pkg/{tests,src} in the build container,
@@ -78,11 +81,45 @@ PLUGIN = textwrap.dedent(
     @pytest.fixture
     def host_device(host_runtime):
         return _cuda_device(host_runtime)
+
+
+    def _cuda_daemon(ndev, locality):
+        # this package's daemon (parcel protocol) serving the B200 — two
+        # logical devices on GPU 0 where the reference's daemon had two sims
+        from paper_1810_11482_b200 import Runtime as CudaRuntime
+        from paper_1810_11482_b200.transport import serve as cuda_serve
+
+        rt = CudaRuntime(devices=[0] * ndev, locality_id=locality)
+        return rt, cuda_serve("127.0.0.1:0", rt)
+
+
+    @pytest.fixture
+    def loopback():
+        # (reference client runtime, daemon): the daemon is this package's,
+        # serving the B200 at locality 9 (reference conftest: a sim daemon)
+        daemon_rt, daemon = _cuda_daemon(2, 9)
+        client = Runtime(backend="sim", devices=1)
+        client.connect(daemon.address)
+        yield client, daemon
+        client.close()
+        daemon.stop()
+        daemon_rt.close()
+
+
+    @pytest.fixture
+    def host_loopback():
+        daemon_rt, daemon = _cuda_daemon(1, 11)
+        client = Runtime(backend="host", devices=1)
+        client.connect(daemon.address)
+        yield client, daemon
+        client.close()
+        daemon.stop()
+        daemon_rt.close()
     """
 )
 
 MODULES = ("test_buffer.py", "test_program.py", "test_device.py", "test_bench.py",
-           "test_acceptance.py", "test_registry.py")
+           "test_acceptance.py", "test_registry.py", "test_transport.py")
 
 
 def main() -> None:

@@ -253,3 +253,22 @@ def test_reference_futures_suite_against_ours(tmp_path):
         env=env, capture_output=True, text=True, timeout=600, cwd=str(tmp_path))
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
+
+
+def test_device_info_equals_reference_snapshot(ref_src):
+    """A daemon's DeviceInfo decoded by the reference client (its own class)
+    equals this package's snapshot of the same device (reference
+    tests/test_transport.py:54-59 compares the two)."""
+    sys.path.insert(0, ref_src)
+    try:
+        from offloadrt.device import DeviceInfo as RefInfo
+    finally:
+        sys.path.remove(ref_src)
+    from paper_1810_11482_b200.device import DeviceInfo
+
+    ours = DeviceInfo("cuda0", (10, 0), 191502876672, 148)
+    ref = RefInfo("cuda0", (10, 0), 191502876672, 148)
+    assert ref == ours and ours == ref and hash(ours) == hash(DeviceInfo("cuda0", (10, 0),
+                                                                         191502876672, 148))
+    assert ours != RefInfo("cuda1", (10, 0), 191502876672, 148)
+    assert ours != ("cuda0", (10, 0), 191502876672, 148)
