@@ -58,3 +58,37 @@ def test_dot_f32_matches_reference(dev):
         ref = case["result"]
         assert abs(got - ref) <= 1e-5 * ref      # BASELINE's stated fp32 tolerance
         assert abs(got - ref) <= 1e-12 * ref     # what fp64 accumulation gives
+
+
+@pytest.mark.parametrize("n,steps", _heat_cases())
+def test_heat_chunks_match_reference(dev, n, steps):
+    """bench.HeatChunks (independent halo-extended pieces, transfers
+    overlapped with the steps) reproduces the reference's field bit for bit."""
+    from paper_1810_11482_b200 import pinned_empty
+    from paper_1810_11482_b200.bench import HeatChunks
+
+    case = next(c for c in _long()["heat"] if c["n"] == n and c["steps"] == steps)
+    x = pinned_empty(n * 8, np.float64)
+    x[:] = np.random.default_rng(case["seed"]).random(n)
+    out = pinned_empty(n * 8, np.float64)
+    HeatChunks(dev, n, steps, chunks=16, sets=3)(x, out)
+    assert hashlib.sha256(out).hexdigest() == case["sha256"]
+
+
+@pytest.mark.parametrize("n,steps,chunks,sets", [
+    (3, 5, 4, 2),          # smaller than one halo: a single piece
+    (1000, 7, 9, 2),       # ragged pieces
+    (4097, 0, 5, 3),       # zero steps: the input comes back
+    (20011, 333, 7, 1),    # one buffer pair for every piece (stream order reuses it)
+    (65536, 1, 64, 4),     # one step, many pieces
+])
+def test_heat_chunks_edge_cases(dev, n, steps, chunks, sets):
+    import oracle
+    from paper_1810_11482_b200 import pinned_empty
+    from paper_1810_11482_b200.bench import HeatChunks
+
+    x = pinned_empty(n * 8, np.float64)
+    x[:] = np.random.default_rng(n + steps).random(n)
+    out = pinned_empty(n * 8, np.float64)
+    HeatChunks(dev, n, steps, chunks=chunks, sets=sets)(x, out)
+    assert np.array_equal(out.view(np.uint64), oracle.heat(np.array(x), steps).view(np.uint64))
