@@ -194,6 +194,11 @@ class CudaDispatch:
         return self._tokenized(lambda: make_ready(self._registry.unregister(gid)))
 
 
+# the reference's name for the local dispatch surface (runtime.py:30-120),
+# so code importing offloadrt.runtime.LocalDispatch switches over unchanged
+LocalDispatch = CudaDispatch
+
+
 class Runtime:
     """One process: its CUDA devices, registry and dispatch table.  Use as a
     context manager or call close()."""
