@@ -243,7 +243,7 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
   if (row_step == 0) return ofl::set_error(OFL_ERR_BAD_ARGS, "row_step must be >= 1");
   const uint64_t total = (uint64_t)((uint32_t)(width * height));  // u32 wrap as mandelbrot.k
   const uint64_t limit = items < total ? items : total;
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:mandelbrot");
   if (!q.ok()) return q.status;
   if (limit && width && row_first < height) {
     MandelArgs a;

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(kThreads) k_partition(double* __restrict__ out
 extern "C" int ofl_partition(ofl_stream* s, double* out, uint32_t offset, uint64_t count,
                              uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:partition");
   if (!q.ok()) return q.status;
   if (count) {
     uint64_t blocks = (count + kThreads - 1) / kThreads;

@@ -225,7 +225,7 @@ extern "C" int ofl_sum_u32(ofl_stream* s, const uint32_t* in, uint32_t* res, uin
   OFL_CHECK_STREAM(s);
   if (reinterpret_cast<uintptr_t>(in) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "sum input must be 16-byte aligned");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:sum_u32");
   if (!q.ok()) return q.status;
   const int blocks = grid_for(s, n >> 2, 4, kSumCtasPerSm);
   void* scratch = nullptr;
@@ -243,7 +243,7 @@ extern "C" int ofl_dot_f32(ofl_stream* s, const float* a, const float* b, double
   OFL_CHECK_STREAM(s);
   if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "dot operands must be 16-byte aligned");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:dot_f32");
   if (!q.ok()) return q.status;
   const int blocks = grid_for(s, n >> 2, 2, kDotCtasPerSm);
   void* scratch = nullptr;
@@ -275,7 +275,7 @@ extern "C" int ofl_dot_f32_allreduce(ofl_stream* s, const float* a, const float*
   pr.rank = rank;
   pr.nranks = nranks;
   pr.round = round;
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:dot_f32_allreduce");
   if (!q.ok()) return q.status;
   const int blocks = grid_for(s, n >> 2, 2, kDotCtasPerSm);
   void* scratch = nullptr;

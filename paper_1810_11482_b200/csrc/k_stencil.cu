@@ -476,7 +476,7 @@ extern "C" int ofl_stencil(ofl_stream* s, const double* x, double* y, uint64_t n
   const uint64_t m = items < n ? items : n;
   if (m && (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil operands must be 16-byte aligned");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:stencil");
   if (!q.ok()) return q.status;
   if (m) {
     launch_stencil(s->cs, x, y, n, m);
@@ -498,7 +498,7 @@ extern "C" int ofl_heat(ofl_stream* s, double* x, double* y, uint64_t n, uint64_
   if (tb < 1 || tb > 128) return ofl::set_error(OFL_ERR_BAD_ARGS, "temporal block must be 1..128");
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat operands must be 16-byte aligned");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:heat");
   if (!q.ok()) return q.status;
   const int sms = ofl::num_sms(s->dev);
   double* src = x;
@@ -562,7 +562,7 @@ extern "C" int ofl_heat_slab(ofl_stream* s, const double* x, double* y, uint64_t
     return ofl::set_error(OFL_ERR_BAD_ARGS, "heat slab operands must be 16-byte aligned");
   if (left_ghost && left_dev != s->dev) ofl::enable_peer(s->dev, left_dev);
   if (right_ghost && right_dev != s->dev) ofl::enable_peer(s->dev, right_dev);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:heat_slab");
   if (!q.ok()) return q.status;
   SlabOut so{(int64_t)own_lo, (int64_t)own_hi, (int64_t)h, h ? left_ghost : nullptr,
              h ? right_ghost : nullptr};

@@ -222,7 +222,7 @@ extern "C" int ofl_stencil2d(ofl_stream* s, const double* x, double* y, uint32_t
                              uint64_t items, uint64_t x_elems, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (x == y && items) return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil2d: x and y must differ");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:stencil2d");
   if (!q.ok()) return q.status;
   const uint64_t cells = (uint64_t)(uint32_t)(w * h);  // u32 wrap as stencil2d.k
   const uint64_t m = items < cells ? items : cells;
@@ -259,7 +259,7 @@ extern "C" int ofl_stencil2d_slab(ofl_stream* s, const double* x, double* y, uin
     return ofl::set_error(OFL_ERR_BAD_ARGS, "stencil2d slab: bad shape or owned rows");
   if (up_ghost && up_dev != s->dev) ofl::enable_peer(s->dev, up_dev);
   if (down_ghost && down_dev != s->dev) ofl::enable_peer(s->dev, down_dev);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:stencil2d_slab");
   if (!q.ok()) return q.status;
   const uint64_t m = (uint64_t)w * h;
   if (m && own_lo < own_hi) {

@@ -160,7 +160,7 @@ extern "C" int ofl_stream_op(ofl_stream* s, int op, double* a, const double* b, 
   if (op < OFL_STREAM_COPY || op > OFL_STREAM_TRIAD)
     return ofl::set_error(OFL_ERR_BAD_ARGS, "unknown STREAM op");
   if (!c) c = b;
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:stream_op");
   if (!q.ok()) return q.status;
   if (n) {
     const cudaError_t e = ofl::stream_launch(s->cs, ofl::num_sms(s->dev), op, a, b, c, scalar, n);

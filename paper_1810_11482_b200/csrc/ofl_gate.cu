@@ -44,7 +44,7 @@ __global__ void k_gate_wait(const unsigned long long* const* counters, int count
 extern "C" int ofl_gate_signal(ofl_stream* s, unsigned long long* counter, uint64_t value,
                                uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:gate_signal");
   if (!q.ok()) return q.status;
   k_gate_signal<<<1, 1, 0, s->cs>>>(counter, value);
   cudaError_t e = cudaPeekAtLastError();
@@ -58,7 +58,7 @@ extern "C" int ofl_gate_wait(ofl_stream* s, const unsigned long long* const* cou
                              uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (count < 0 || count > 64) return ofl::set_error(OFL_ERR_BAD_ARGS, "gate: 0..64 counters");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:gate_wait");
   if (!q.ok()) return q.status;
   if (count) {
     k_gate_wait<<<1, 1, 0, s->cs>>>(counters_dev, count, target, status);

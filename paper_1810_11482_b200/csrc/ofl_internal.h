@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -77,14 +78,26 @@ int stream_scratch(ofl_stream* s, size_t bytes, void** out);
 
 // RAII: locks the stream, makes its device current; finish() assigns the
 // ticket after the CUDA call(s) succeeded.
+// Every stream operation enqueues under its stream's lock and takes the next
+// ticket.  It is also an NVTX range named after the entry point ("ofl:heat",
+// "ofl:stream_op", ...), so nsys timelines and `ncu --nvtx --nvtx-include`
+// filters see the runtime's operations; NVTX3 is header-only and a no-op
+// unless a profiler injects itself.
 struct Enqueue {
   ofl_stream* s;
   std::unique_lock<std::mutex> lk;
   int status = OFL_OK;
-  explicit Enqueue(ofl_stream* st) : s(st), lk(st->mu) {
+  const char* what;
+  explicit Enqueue(ofl_stream* st, const char* name = nullptr) : s(st), lk(st->mu), what(name) {
+    if (what) nvtxRangePushA(what);
     cudaError_t e = use_device(st->dev);
     if (e != cudaSuccess) status = cuda_error(e, "cudaSetDevice");
   }
+  ~Enqueue() {
+    if (what) nvtxRangePop();
+  }
+  Enqueue(const Enqueue&) = delete;
+  Enqueue& operator=(const Enqueue&) = delete;
   bool ok() const { return status == OFL_OK; }
   int finish(uint64_t* ticket) {
     cudaError_t e = cudaGetLastError();

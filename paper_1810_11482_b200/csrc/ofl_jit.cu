@@ -120,7 +120,7 @@ int ofl_jit_launch(ofl_stream* s, ofl_jit* k, void** params, uint64_t blocks, in
                    uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (!k) return ofl::set_error(OFL_ERR_BAD_ARGS, "null jit kernel");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:jit_launch");
   if (!q.ok()) return q.status;
   if (blocks) {
     cudaError_t e = cudaLaunchKernel((const void*)k->kern, dim3((unsigned)blocks), dim3(threads),
@@ -142,7 +142,7 @@ int ofl_jit_destroy(ofl_jit* k) {
 // 0xFF-fill `bytes` of device memory on the stream (error-record reset)
 int ofl_fill_ones(ofl_stream* s, void* dptr, uint64_t bytes, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:fill_ones");
   if (!q.ok()) return q.status;
   cudaError_t e = cudaMemsetAsync(dptr, 0xFF, bytes, s->cs);
   if (e != cudaSuccess) return ofl::cuda_error(e, "memset");

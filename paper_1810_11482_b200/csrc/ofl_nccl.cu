@@ -133,7 +133,7 @@ int ofl_allreduce(ofl_comm* c, ofl_stream* s, const void* send, void* recv, uint
   ncclRedOp_t ro;
   if (!dtype_of(dtype, &dt) || !op_of(op, &ro))
     return ofl::set_error(OFL_ERR_BAD_ARGS, "unsupported allreduce dtype/op");
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:allreduce");
   if (!q.ok()) return q.status;
   ncclResult_t r = g_api.AllReduce(send, recv, count, dt, ro, c->comm, s->cs);
   if (r != ncclSuccess) return nccl_error(r, "ncclAllReduce");

@@ -568,7 +568,7 @@ int ofl_host_free(void* hptr) {
 static int copy_op(ofl_stream* s, void* dst, const void* src, uint64_t bytes, cudaMemcpyKind k,
                    uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
-  Enqueue q(s);
+  Enqueue q(s, "ofl:copy");
   if (!q.ok()) return q.status;
   if (bytes) {
     cudaError_t e = cudaMemcpyAsync(dst, src, bytes, k, s->cs);
@@ -587,7 +587,7 @@ int ofl_d2h_rows(ofl_stream* s, void* dst, uint64_t dst_pitch, const void* src,
                  uint64_t row_bytes, uint64_t rows, uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   if (dst_pitch < row_bytes) return set_error(OFL_ERR_BAD_ARGS, "destination pitch < row bytes");
-  Enqueue q(s);
+  Enqueue q(s, "ofl:d2h_rows");
   if (!q.ok()) return q.status;
   if (row_bytes && rows) {
     // contiguous rows: one linear DMA (a 2-D copy pays per row)
@@ -609,7 +609,7 @@ int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev,
   if (dst_dev == src_dev) return copy_op(s, dst, src, bytes, cudaMemcpyDeviceToDevice, ticket);
   enable_peer(dst_dev, src_dev);
   enable_peer(src_dev, dst_dev);
-  Enqueue q(s);
+  Enqueue q(s, "ofl:p2p");
   if (!q.ok()) return q.status;
   if (bytes) {
     cudaError_t e = cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes, s->cs);

@@ -241,7 +241,7 @@ extern "C" int ofl_h2d_pageable(ofl_stream* s, void* dst, const void* src, uint6
                                 uint64_t* ticket) {
   OFL_CHECK_STREAM(s);
   std::lock_guard<std::mutex> ring_lock(g_ring.mu);
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:h2d_pageable");
   if (!q.ok()) return q.status;
   const uint64_t nchunks = (bytes + kSlotBytes - 1) / kSlotBytes;
   auto len_of = [&](uint64_t k) {
@@ -283,7 +283,7 @@ extern "C" int ofl_d2h_chunked(ofl_stream* s, void* staging, const void* src, ui
   if (!out || !staging || !chunk) return ofl::set_error(OFL_ERR_BAD_ARGS, "d2h_chunked arguments");
   *out = nullptr;
   auto* r = new ofl_read{s->dev, (const char*)staging, bytes, chunk, {}};
-  ofl::Enqueue q(s);
+  ofl::Enqueue q(s, "ofl:d2h_chunked");
   if (!q.ok()) {
     delete r;
     return q.status;
