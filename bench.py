@@ -1031,11 +1031,12 @@ def run_ours(args) -> None:
             if finished.wait(args.configs_budget):
                 return
             if rank == 0:
+                done = dict(configs)  # one C-level copy: the main thread may still insert
                 for name in names:
-                    configs.setdefault(name, {"error": f"not finished within --configs-budget "
-                                                       f"{args.configs_budget:g} s"})
-                configs["overhead"] = overhead
-                print(json.dumps(line), flush=True)
+                    done.setdefault(name, {"error": f"not finished within --configs-budget "
+                                                    f"{args.configs_budget:g} s"})
+                done["overhead"] = overhead
+                print(json.dumps(dict(line, configs=done)), flush=True)
             os._exit(0)
 
         threading.Thread(target=watchdog, daemon=True).start()
