@@ -142,7 +142,11 @@ int ofl_read_release(ofl_read* r);
 int ofl_p2p(ofl_stream* s, void* dst, int dst_dev, const void* src, int src_dev,
             uint64_t bytes, uint64_t* ticket);
 /* device-side ordering: `waiter` does not run past this point until `on`
- * has completed `ticket` (cudaStreamWaitEvent on a lazily placed marker) */
+ * has completed `ticket` (cudaStreamWaitEvent on a lazily placed marker).
+ * With no marker at or after `ticket` yet, one is recorded at `on`'s tail,
+ * so a wait on an older ticket also waits for the work enqueued since;
+ * `waiter == on` only places that marker — called right after enqueueing,
+ * it pins an exact marker for a later wait. */
 int ofl_stream_wait(ofl_stream* waiter, ofl_stream* on, uint64_t ticket);
 
 /* ---- completion: replaces Promise fulfilment by the stream worker

@@ -220,35 +220,77 @@ struct SlabOut {
   double* right;  // receives y[own_hi - h, own_hi), or null
 };
 
-template <int R, bool kSlab>
-__device__ __noinline__ void heat_tile_slow(const double* __restrict__ x, double* __restrict__ y,
-                                            int64_t nn, int tb, bool fma_ok, int64_t g0, int lane,
-                                            int64_t own_lo, int64_t own_hi, int64_t h,
-                                            double* left, double* right) {
-  constexpr int kCells = 32 * R;
-  double a[R], b[R];
+// Cells per lane of the windows the general path advances (below): 32*kSlowR
+// cells fit two register arrays without spilling, and exceed 2*tb (tb <= 128).
+constexpr int kSlowR = 32;
+
+// tb steps of one window of 32*RS consecutive cells starting at w0 >= 0, in
+// registers (lane l holds cells w0 + l*RS ...); cells [vlo, vhi) are stored.
+// A window flush with the field's start (w0 == 0) holds global cell 0 at
+// lane 0 / index 0, one flush with its end holds cell n-1 at lane 31 /
+// index RS-1: those cells are put back after every step (one predicated move,
+// no per-cell edge test), and since a fixed cell never reads its outer
+// neighbour, nothing beyond it matters.  Only a field shorter than the window
+// takes the per-cell edge test (cells past n-1 are zeros nobody reads).
+template <int RS, bool kSlab>
+__device__ __noinline__ void heat_window(const double* __restrict__ x, double* __restrict__ y,
+                                         int64_t nn, int tb, bool fma_ok, int64_t w0, int64_t vlo,
+                                         int64_t vhi, int lane, int64_t own_lo, int64_t own_hi,
+                                         int64_t h, double* left, double* right) {
+  constexpr int64_t kW = 32 * RS;
+  const int64_t g0 = w0 + (int64_t)lane * RS;
+  double a[RS], b[RS];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t g = g0 + i;
-    a[i] = (g >= 0 && g < nn) ? x[g] : 0.0;
-  }
+  for (int i = 0; i < RS; ++i) a[i] = g0 + i < nn ? __ldg(x + g0 + i) : 0.0;
   bool fused = fma_ok;
   if (fused) {
     const uint64_t lo_bits = (uint64_t)(tb + 3) << 52;  // 2^(tb-1020), see warp_tile_steps
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
+    for (int i = 0; i < RS; ++i) {
       const uint64_t u = (uint64_t)__double_as_longlong(a[i]);
       fused &= (u == 0) || (u >= lo_bits && u < 0x8000000000000000ull);
     }
   }
   fused = __all_sync(0xffffffffu, fused);
-  const bool odd = fused ? warp_steps<R, true, true>(a, b, lane, g0, nn, tb)
-                         : warp_steps<R, false, true>(a, b, lane, g0, nn, tb);
+  bool odd;
+  if (w0 + kW > nn) {  // the whole field inside one window
+    odd = fused ? warp_steps<RS, true, true>(a, b, lane, g0, nn, tb)
+                : warp_steps<RS, false, true>(a, b, lane, g0, nn, tb);
+  } else {
+    const bool fix_lo = w0 == 0 && lane == 0;
+    const bool fix_hi = w0 + kW == nn && lane == 31;
+    int st = 0;
+    for (; st + 1 < tb; st += 2) {
+      if (fused) {
+        warp_step<RS, true, false>(a, b, lane, g0, nn);
+      } else {
+        warp_step<RS, false, false>(a, b, lane, g0, nn);
+      }
+      if (fix_lo) b[0] = a[0];
+      if (fix_hi) b[RS - 1] = a[RS - 1];
+      if (fused) {
+        warp_step<RS, true, false>(b, a, lane, g0, nn);
+      } else {
+        warp_step<RS, false, false>(b, a, lane, g0, nn);
+      }
+      if (fix_lo) a[0] = b[0];
+      if (fix_hi) a[RS - 1] = b[RS - 1];
+    }
+    odd = st < tb;
+    if (odd) {
+      if (fused) {
+        warp_step<RS, true, false>(a, b, lane, g0, nn);
+      } else {
+        warp_step<RS, false, false>(a, b, lane, g0, nn);
+      }
+      if (fix_lo) b[0] = a[0];
+      if (fix_hi) b[RS - 1] = a[RS - 1];
+    }
+  }
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int local = lane * R + i;
+  for (int i = 0; i < RS; ++i) {
     const int64_t g = g0 + i;
-    if (local >= tb && local < kCells - tb && g >= 0 && g < nn) {
+    if (g >= vlo && g < vhi) {
       const double v = odd ? b[i] : a[i];
       if (!kSlab) {
         y[g] = v;
@@ -258,6 +300,40 @@ __device__ __noinline__ void heat_tile_slow(const double* __restrict__ x, double
         if (right && g >= own_hi - h) right[g - (own_hi - h)] = v;
       }
     }
+  }
+}
+
+// The general path for a whole tile (cells [c_lo, c_hi) after tb steps):
+// tiles at the field's ends, overhanging it, or (slab passes) reaching the
+// strips sent to the neighbours.  The range is covered by windows of
+// 32*kSlowR cells — flush with cell 0 / n-1 where the tile touches them,
+// else with tb halo cells each side — so the general path never holds a
+// 32*R-cell tile in registers (which spilled and made these few tiles the
+// critical path of a short pass: a ~0.3 ms floor per pass).
+template <int R, bool kSlab>
+__device__ __forceinline__ void heat_tile_slow(const double* __restrict__ x, double* __restrict__ y,
+                                               int64_t nn, int tb, bool fma_ok, int64_t c_lo,
+                                               int64_t c_hi, int lane, int64_t own_lo,
+                                               int64_t own_hi, int64_t h, double* left,
+                                               double* right) {
+  constexpr int64_t kW = 32 * kSlowR;
+  int64_t pos = c_lo;
+  while (pos < c_hi) {
+    int64_t w0, end;
+    if (nn <= kW || pos <= tb) {  // flush with cell 0 (or the field is one window)
+      w0 = 0;
+      end = nn <= kW ? nn : kW - tb;
+    } else if (pos - tb + kW >= nn) {  // flush with cell n-1
+      w0 = nn - kW;
+      end = nn;
+    } else {
+      w0 = pos - tb;
+      end = pos + kW - 2 * tb;
+    }
+    const int64_t hi = end < c_hi ? end : c_hi;
+    heat_window<kSlowR, kSlab>(x, y, nn, tb, fma_ok, w0, pos, hi, lane, own_lo, own_hi, h, left,
+                               right);
+    pos = hi;
   }
 }
 
@@ -376,7 +452,8 @@ __global__ void __launch_bounds__(kWarpThreads, heat_pipe_min_blocks<R>())
   int64_t k = grab();
   while (k < n_edge) {  // edge / overhanging tiles: general path, global memory
     const int64_t te = tile_of(k);
-    heat_tile_slow<R, kSlab>(x, y, nn, tb, fma_ok, te * valid - tb + (int64_t)lane * R, lane,
+    heat_tile_slow<R, kSlab>(x, y, nn, tb, fma_ok, te * valid,
+                             te * valid + valid < nn ? te * valid + valid : nn, lane,
                              so.own_lo, so.own_hi, so.h, so.left, so.right);
     k = grab();
   }

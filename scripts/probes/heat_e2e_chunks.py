@@ -28,7 +28,8 @@ def main() -> None:
         x = pinned_empty(n * 8, np.float64)
         x[:] = np.random.default_rng(20180214).random(n)
         out = pinned_empty(n * 8, np.float64)
-        combos = [tuple(map(int, c.split("x"))) for c in os.environ.get("COMBOS", "8x2,8x3,16x2,16x3,16x4,32x3,32x4,64x3").split(",")]
+        combos = [tuple(map(int, c.split("x"))) for c in
+                  os.environ.get("COMBOS", "8x2,8x3,16x2,16x3,16x4,24x6,32x3,32x4,64x3").split(",")]
         for chunks, sets in combos:
             hc = HeatChunks(dev, n, steps, chunks=chunks, sets=sets)
             ts = []

@@ -92,3 +92,16 @@ def test_heat_chunks_edge_cases(dev, n, steps, chunks, sets):
     out = pinned_empty(n * 8, np.float64)
     HeatChunks(dev, n, steps, chunks=chunks, sets=sets)(x, out)
     assert np.array_equal(out.view(np.uint64), oracle.heat(np.array(x), steps).view(np.uint64))
+
+
+def test_heat_chunks_pageable_host_arrays(dev):
+    """Plain numpy arrays in and out (staged writes, chunked reads into the
+    caller's array), two buffer pairs reused in stream order."""
+    import oracle
+    from paper_1810_11482_b200.bench import HeatChunks
+
+    n, steps = 3 << 20, 40
+    x = np.random.default_rng(11).random(n)
+    out = np.zeros(n)
+    HeatChunks(dev, n, steps, chunks=12, sets=2)(x, out)
+    assert np.array_equal(out.view(np.uint64), oracle.heat(x.copy(), steps).view(np.uint64))
