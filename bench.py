@@ -930,7 +930,7 @@ def run_ours(args) -> None:
                              + (dev.create_stream(),) for _ in range(nsets - 1)]
     outs = [a_host] + [pinned_empty(n * 8, np.float64) for _ in range(nsets - 1)]
 
-    def e2e(steps: int) -> None:
+    def e2e(steps: int, compute: bool = True) -> None:
         pending = []
         for k in range(steps):
             Ak, Bk, Ck, sk = sets[k % nsets]
@@ -938,16 +938,22 @@ def run_ours(args) -> None:
                 pending.pop(0).get()
             Bk.enqueue_write(0, b_host, sk)
             Ck.enqueue_write(0, c_host, sk)
-            prog.run([Ak, Bk, Ck, s, n], "triad", grid, block, sk)
+            if compute:
+                prog.run([Ak, Bk, Ck, s, n], "triad", grid, block, sk)
             pending.append(Ak.enqueue_read_into(0, outs[k % nsets], sk))
         for t in pending:
             t.get()
 
-    e2e(4)
-    dist.barrier()
-    t0 = time.perf_counter()
-    e2e(args.e2e_steps)
-    e2e_s = dist.max(time.perf_counter() - t0)
+    def timed_e2e(compute: bool) -> float:
+        e2e(4, compute)
+        dist.barrier()
+        t0 = time.perf_counter()
+        e2e(args.e2e_steps, compute)
+        return dist.max(time.perf_counter() - t0)
+
+    # the same copies with no kernel: the host link's floor for this schedule
+    link_s = timed_e2e(False)
+    e2e_s = timed_e2e(True)
     e2e_value = world * step_bytes * args.e2e_steps / e2e_s / 1e9
     for o in outs:
         if not np.array_equal(o.view(np.uint64), expect.view(np.uint64)):
@@ -1003,8 +1009,11 @@ def run_ours(args) -> None:
             "d2h_bytes_per_step": n * 8,
             "steps": args.e2e_steps,
             "ms_per_step": round(e2e_s / args.e2e_steps * 1e3, 3),
+            "link_floor_ms_per_step": round(link_s / args.e2e_steps * 1e3, 3),
+            "frac_of_link_floor": round(link_s / e2e_s, 4),
             "schedule": "write b, write c (pinned), run, read_into a (pinned) per step; "
-            f"steps rotate over {nsets} streams x {nsets} device buffer sets; wall clock",
+            f"steps rotate over {nsets} streams x {nsets} device buffer sets; wall clock; "
+            "link floor = the same writes and reads with no kernel",
         },
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
