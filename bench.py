@@ -490,6 +490,16 @@ def config_heat(rt, dev, lib, fp64: float, n: int = 1 << 28, steps: int = 1000) 
         e2e.append(time.perf_counter() - t0)
     digest_chunked = _sha(xout)
     del chunked
+    # the host-link floor of that schedule: the same pieces written and read
+    # with zero steps (HeatChunks with steps=0: no halo, no kernel work)
+    copies = HeatChunks(dev, n, 0)
+    floor = []
+    for _ in range(3):
+        dev.synchronize().get()
+        t0 = time.perf_counter()
+        when_all(copies.enqueue(x, xout)).get()
+        floor.append(time.perf_counter() - t0)
+    del copies
     kernel = []
     for _ in range(3):  # device time of the steps alone (input re-written, untimed)
         X.enqueue_write(0, x)
@@ -508,6 +518,8 @@ def config_heat(rt, dev, lib, fp64: float, n: int = 1 << 28, steps: int = 1000) 
         "fp64_peak_ops_per_s": round(fp64, 1),
         "frac_fp64": round(useful / (ms * 1e-3) / fp64, 4) if fp64 else None,
         "e2e_ms_pinned_host": round(min(e2e) * 1e3, 2),
+        "e2e_link_floor_ms": round(min(floor) * 1e3, 2),
+        "e2e_frac_of_link_floor": round(min(floor) / min(e2e), 4),
         "e2e_schedule": "bench.HeatChunks: 24 halo-extended pieces over 6 buffer pairs / streams, "
                         "write / 1000 steps / read of successive pieces overlapped",
         "e2e_ms_sequential": round(min(mono) * 1e3, 2),
@@ -561,11 +573,18 @@ def config_mandelbrot(rt, dev, lib, fp64: float) -> dict:
         when_all(tiles.enqueue()).get()
         e2e.append(time.perf_counter() - t0)
     ok_e2e = ref is not None and _sha(tiles.image) == ref["sha256"]
+    floor = []  # the image read alone (one D2H into pinned memory): the link floor
+    for _ in range(5):
+        t0 = time.perf_counter()
+        O.enqueue_read_into(0, host).get()
+        floor.append(time.perf_counter() - t0)
     return {
         "workload": "Mandelbrot 7680x4320 max_iter 2000 (BASELINE config 3), 1 GPU",
         "kernel_ms": round(ms, 3),
         "e2e_ms_overlapped_into_pinned_image": round(min(e2e) * 1e3, 3),
         "e2e_d2h_bytes": w * h * 4,
+        "e2e_link_floor_ms": round(min(floor) * 1e3, 3),
+        "e2e_frac_of_link_floor": round(min(floor) / min(e2e), 4),
         "reference_dp_ops": dp_ops,
         "reference_op_rate_over_fp64_peak": round(dp_ops / (ms * 1e-3) / fp64, 4) if fp64 else None,
         "note": "exact shortcuts (cycle detection; pixels provably inside the main cardioid "
@@ -859,6 +878,11 @@ def run_ours(args) -> None:
     ngpu = _native.device_count()
     ordinal = local_rank % max(1, ngpu)  # > GPUs ranks only in plumbing tests
     oversubscribed = world > ngpu
+    # threads and pinned staging next to this GPU (one rank per GPU on a
+    # multi-socket host); nothing to do on a single NUMA node
+    from paper_1810_11482_b200.device import bind_host_to_device
+
+    host_binding = None if oversubscribed else bind_host_to_device(ordinal)
     rt = Runtime(devices=[ordinal])
     dev = rt.get_all_devices().get()[0]
     A, B, C = (dev.create_buffer(n * 8).get() for _ in range(3))
@@ -1016,6 +1040,7 @@ def run_ours(args) -> None:
             "link floor = the same writes and reads with no kernel",
         },
         "cpu_baseline": cpu,
+        "host_binding": host_binding or "unchanged (the GPU's local CPUs are all allowed, or unknown)",
         "gpu_launches": int(launches),
         "clocks": clocks,
         "clocks_per_rank": clocks_per_rank if world > 1 else None,

@@ -68,6 +68,9 @@ uint64_t ofl_kernel_launches(void);
 int ofl_device_count(int* count);
 int ofl_device_props(int dev, char* name, int name_cap, int* cc_major, int* cc_minor,
                      uint64_t* mem_bytes, int* sms, uint64_t* l2_bytes);
+/* PCI address "dddd:bb:dd.f" (lower case, as in /sys/bus/pci/devices): the
+ * host side binds a GPU's process to the CPUs / NUMA node nearest to it */
+int ofl_device_pci_bus_id(int dev, char* out, int cap);
 
 /* ---- streams: replaces DeviceObject.create_stream / _StreamWorker
  *      (device.py:129-157,232-233) ---------------------------------------- */

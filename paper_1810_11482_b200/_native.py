@@ -51,6 +51,7 @@ _SIGNATURES = {
         c_int,
         [c_int, c_char_p, c_int, POINTER(c_int), POINTER(c_int), _u64p, POINTER(c_int), _u64p],
     ),
+    "ofl_device_pci_bus_id": (c_int, [c_int, c_char_p, c_int]),
     "ofl_stream_create": (c_int, [c_int, POINTER(c_void_p)]),
     "ofl_stream_destroy": (c_int, [_c_stream]),
     "ofl_stream_tail": (c_uint64, [_c_stream]),

@@ -9,6 +9,7 @@
 #include <sys/eventfd.h>
 #include <unistd.h>
 
+#include <cctype>
 #include <cerrno>
 #include <cstdio>
 #include <cstring>
@@ -296,6 +297,14 @@ int ofl_device_props(int dev, char* name, int name_cap, int* cc_major, int* cc_m
   if (mem_bytes) *mem_bytes = p.totalGlobalMem;
   if (sms) *sms = p.multiProcessorCount;
   if (l2_bytes) *l2_bytes = (uint64_t)p.l2CacheSize;
+  return OFL_OK;
+}
+
+int ofl_device_pci_bus_id(int dev, char* out, int cap) {
+  if (!out || cap < 13) return set_error(OFL_ERR_BAD_ARGS, "pci bus id: buffer of >= 13 bytes");
+  cudaError_t e = cudaDeviceGetPCIBusId(out, cap, dev);
+  if (e != cudaSuccess) return cuda_error(e, "cudaDeviceGetPCIBusId");
+  for (char* c = out; *c; ++c) *c = (char)std::tolower((unsigned char)*c);
   return OFL_OK;
 }
 

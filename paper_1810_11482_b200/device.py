@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes
 import itertools
+import os
 import threading
 from collections import deque
 from dataclasses import dataclass
@@ -85,6 +86,53 @@ def query_physical(ordinal: int) -> PhysicalInfo:
     return PhysicalInfo(
         ordinal, name.value.decode(), (major.value, minor.value), mem.value, sms.value, l2.value
     )
+
+
+def pci_bus_id(ordinal: int) -> str:
+    """The GPU's PCI address as sysfs spells it ("0000:1b:00.0")."""
+    buf = ctypes.create_string_buffer(64)
+    _native.check(_native.load().ofl_device_pci_bus_id(ordinal, buf, 64), "pci bus id")
+    return buf.value.decode()
+
+
+def _cpulist(text: str) -> set:
+    cpus: set = set()
+    for part in text.strip().split(","):
+        if part:
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+    return cpus
+
+
+def local_cpus(ordinal: int, sysfs: str = "/sys/bus/pci/devices") -> Optional[set]:
+    """CPUs of the GPU's NUMA node (sysfs ``local_cpulist``), or None when the
+    platform does not say."""
+    try:
+        with open(os.path.join(sysfs, pci_bus_id(ordinal), "local_cpulist")) as f:
+            return _cpulist(f.read()) or None
+    except (OSError, ValueError):
+        return None
+
+
+def bind_host_to_device(ordinal: int) -> Optional[dict]:
+    """Restrict this process's threads (present and future) to the CPUs
+    nearest to GPU `ordinal`, so pinned staging memory allocated afterwards
+    lands on that NUMA node and the copy threads run next to its PCIe root
+    (one process per GPU on a multi-socket host).  A no-op (None) when the
+    GPU's CPUs are unknown or already all we may use."""
+    cpus = local_cpus(ordinal)
+    if not cpus or not hasattr(os, "sched_setaffinity"):
+        return None
+    allowed = os.sched_getaffinity(0)
+    use = cpus & allowed
+    if not use or use == allowed:
+        return None
+    for tid in os.listdir("/proc/self/task"):
+        try:
+            os.sched_setaffinity(int(tid), use)
+        except OSError:
+            pass  # a thread that exited meanwhile
+    return {"pci_bus_id": pci_bus_id(ordinal), "cpus": len(use), "of": len(allowed)}
 
 
 class Stream:

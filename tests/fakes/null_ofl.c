@@ -18,6 +18,8 @@ uint64_t ofl_kernel_launches(void) { return launches; }
 int ofl_device_count(int* c) { *c = 1; return 0; }
 int ofl_device_props(int d, char* name, int cap, int* ma, int* mi, uint64_t* mem, int* sms, uint64_t* l2) {
   (void)d; strncpy(name, "null", cap); *ma = 10; *mi = 0; *mem = 1ull << 37; *sms = 148; *l2 = 1 << 27; return 0; }
+int ofl_device_pci_bus_id(int d, char* out, int cap) {
+  (void)d; if (!out || cap < 13) return 2; strncpy(out, "0000:00:00.0", cap); return 0; }
 int ofl_stream_create(int d, void** out) { (void)d; *out = calloc(1, sizeof(S)); return 0; }
 int ofl_stream_destroy(void* s) { free(s); return 0; }
 uint64_t ofl_stream_tail(void* s) { return ((S*)s)->tail; }

@@ -565,3 +565,18 @@ def test_launch_and_write_plans_track_arguments(rt, dev):
     rt.registry.unregister(C.gid)
     with pytest.raises(UnknownGidError):
         prog.run(args, "triad", grid, block).get()
+
+
+@pytest.mark.gpu
+def test_pci_bus_id_and_local_cpus():
+    """The GPU's PCI address names its sysfs node; its CPU list (if the
+    platform reports one) intersects the CPUs this process may use."""
+    import os
+
+    from paper_1810_11482_b200 import device
+
+    bus = device.pci_bus_id(0)
+    assert len(bus) == 12 and bus == bus.lower() and bus[4] == ":" and bus[10] == "."
+    cpus = device.local_cpus(0)
+    if os.path.isdir(os.path.join("/sys/bus/pci/devices", bus)) and cpus is not None:
+        assert cpus & os.sched_getaffinity(0)

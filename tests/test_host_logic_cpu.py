@@ -251,3 +251,44 @@ def test_oflcall_module_against_null_abi(fake_lib, tmp_path):
     r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OFLCALL OK" in r.stdout
+
+
+BIND_SCRIPT = textwrap.dedent(
+    r"""
+    import os, sys, tempfile
+    sys.path.insert(0, REPO_PATH)
+    from paper_1810_11482_b200 import device
+    assert device._cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert device._cpulist("") == set()
+    assert device.pci_bus_id(0) == "0000:00:00.0"          # the null ABI's address
+    root = tempfile.mkdtemp()
+    assert device.local_cpus(0, sysfs=root) is None         # no sysfs entry: unknown
+    os.makedirs(os.path.join(root, "0000:00:00.0"))
+    allowed = sorted(os.sched_getaffinity(0))
+    with open(os.path.join(root, "0000:00:00.0", "local_cpulist"), "w") as f:
+        f.write(",".join(map(str, allowed)))
+    assert device.local_cpus(0, sysfs=root) == set(allowed)
+    # the GPU's CPUs are everything we may use: nothing to bind
+    device.local_cpus = lambda o, sysfs=None: set(allowed)
+    assert device.bind_host_to_device(0) is None
+    if len(allowed) > 1:
+        device.local_cpus = lambda o, sysfs=None: {allowed[0]}
+        info = device.bind_host_to_device(0)
+        assert info == {"pci_bus_id": "0000:00:00.0", "cpus": 1, "of": len(allowed)}, info
+        assert os.sched_getaffinity(0) == {allowed[0]}
+    device.local_cpus = lambda o, sysfs=None: {10 ** 6}     # none of them allowed
+    assert device.bind_host_to_device(0) is None
+    print("BIND OK")
+    """
+)
+
+
+def test_bind_host_to_device_against_null_abi(fake_lib):
+    """NUMA-local host binding (bench.py, one rank per GPU): sysfs cpulist
+    parsing, no-op when the GPU's CPUs are all allowed or unknown, every
+    thread restricted otherwise."""
+    env = dict(os.environ, OFL_LIB=fake_lib)
+    r = subprocess.run([sys.executable, "-c", BIND_SCRIPT.replace("REPO_PATH", repr(REPO))],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "BIND OK" in r.stdout
