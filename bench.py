@@ -622,10 +622,13 @@ def config_dot(rt, dev, lib, n: int = 1 << 31) -> dict:
         e2e.append(time.perf_counter() - t0)
     t = EventTimer(lib, st, dev_ordinal(rt))
     K = 10
-    t.start()
-    for _ in range(K):
-        prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
-    ms = t.stop() / K
+    batches = []
+    for _ in range(3):  # best of 3 batches of K back-to-back launches
+        t.start()
+        for _ in range(K):
+            prog.run([A, B, R, n], "dot_f32", grid, (256, 1, 1))
+        batches.append(t.stop() / K)
+    ms = min(batches)
     exp = oracle.dot_f32(a, b, threads=0)
     rel = abs(got - exp) / abs(exp)
     gbs = 8.0 * n / (ms * 1e-3) / 1e9
