@@ -19,6 +19,8 @@ with Runtime(devices=[0]) as rt:
     bp.run([X, Y, n, 130], "heat", *g).get()          # fused path
     X.enqueue_write(0, rng.standard_normal(n))
     bp.run([X, Y, n, 65], "heat", *g).get()           # unfused path + split pass
+    for m in (700, 1024, 1500):                        # general-path windows: one window,
+        bp.run([X, Y, m, 20], "heat", *g).get()       # exactly one, flush at both ends
     for op in ("copy", "scale", "add", "triad"):
         p = d.create_program_with_source(kernel_source("stream")).get()
         p.build(op).get()
