@@ -362,6 +362,29 @@ def test_c_abi_example_runs(tmp_path):
     assert "0 mismatches" in r.stdout
 
 
+def test_python_examples_run():
+    """examples/listing2_sum.py (the paper's workflow listing on this API) and,
+    when the reference package is installed in baseline/_ref,
+    examples/reference_runtime_on_b200.py (the unmodified reference runtime
+    driving the B200 through offloadrt_backend.attach)."""
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(repo, "examples", "listing2_sum.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert ": 1000" in r.stdout
+    ref = os.path.join(repo, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "offloadrt")):
+        pytest.skip("reference package not installed (baseline/_ref)")
+    env = dict(os.environ, PYTHONPATH=ref + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, os.path.join(repo, "examples", "reference_runtime_on_b200.py")],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "matches numpy" in r.stdout
+
+
 IPC_HEAT_SCRIPT = r"""
 import sys
 sys.path.insert(0, sys.argv[1])
