@@ -520,7 +520,7 @@ def config_heat(rt, dev, lib, fp64: float, n: int = 1 << 28, steps: int = 1000) 
         "e2e_ms_pinned_host": round(min(e2e) * 1e3, 2),
         "e2e_link_floor_ms": round(min(floor) * 1e3, 2),
         "e2e_frac_of_link_floor": round(min(floor) / min(e2e), 4),
-        "e2e_schedule": "bench.HeatChunks: 24 halo-extended pieces over 6 buffer pairs / streams, "
+        "e2e_schedule": "bench.HeatChunks: 64 halo-extended pieces over 12 buffer pairs / streams, "
                         "write / 1000 steps / read of successive pieces overlapped",
         "e2e_ms_sequential": round(min(mono) * 1e3, 2),
         "e2e_h2d_bytes": n * 8, "e2e_d2h_bytes": n * 8,

@@ -837,12 +837,17 @@ class HeatChunks:
     (2 x n x 8 bytes, both directions busy) rather than the sum of copy and
     compute sets the pace.  Redundant work: 2 x steps cells per inner cut.
     Config 2 on one B200: 108.6 ms written, stepped and read in sequence,
-    54-56 ms with 16-32 pieces over 6-8 pairs (profiles/r02_heat_e2e.txt).
+    54-56 ms with 16-32 pieces over 6-8 pairs (profiles/r02_heat_e2e.txt);
+    once short fields stopped paying a per-pass floor, 51-53 ms with 64
+    pieces over 12 pairs, against ~45 ms for the same copies with no steps
+    (profiles/r02_heat_small_fields.txt).  The pieces' steps must run
+    concurrently: one compute stream running them in order (a write / step
+    / read stream each) took 70 ms, small fields alone leave SMs idle.
 
     ``x`` and ``out`` are pinned float64 arrays of n cells (``pinned_empty``),
     read and written by DMA in place."""
 
-    def __init__(self, device: DeviceHandle, n: int, steps: int, chunks: int = 24, sets: int = 6):
+    def __init__(self, device: DeviceHandle, n: int, steps: int, chunks: int = 64, sets: int = 12):
         if n < 3 or steps < 0 or chunks < 1 or sets < 1:
             raise BadArgsError("heat chunks: n >= 3, steps >= 0, chunks >= 1, sets >= 1")
         chunks = max(1, min(chunks, n // max(1, 2 * steps) or 1, n))
