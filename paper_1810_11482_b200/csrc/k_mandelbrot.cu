@@ -182,10 +182,10 @@ __device__ __forceinline__ bool fused_ok(const double (&cr)[P], const double (&c
 }
 
 // ILP-P variant: lane l handles the same position of the P tiles of a unit.
-// PERIOD keeps two more saved doubles per pixel; capping it at 3 CTAs/SM
-// (85 registers) keeps the occupancy of the plain kernel
+// PERIOD keeps two more saved doubles per pixel; its launch bound asks for 4
+// CTAs/SM (at P = 2 the registers fit without spilling)
 template <bool INTCMP, int P, bool PERIOD = false>
-__global__ void __launch_bounds__(kThreads, PERIOD ? 3 : 1) k_mandelbrotP(MandelArgs a,
+__global__ void __launch_bounds__(kThreads, PERIOD ? 4 : 1) k_mandelbrotP(MandelArgs a,
                                                                        unsigned int* queue) {
   static_assert(kTilesPerUnit % P == 0, "P must divide the unit");
   const int lane = threadIdx.x & 31;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, PERIOD ? 3 : 1) k_mandelbrotP(Mandel
         const uint32_t ty = (uint32_t)(tile / a.tiles_x);
         const uint32_t tx = (uint32_t)(tile % a.tiles_x);
         const uint32_t px = tx * kTileW + (lane & (kTileW - 1));
-        const uint32_t r = ty * kTileH + (lane >> 3);
+        const uint32_t r = ty * kTileH + (lane / kTileW);
         const uint32_t py = a.row_first + r * a.row_step;
         const uint64_t gtid = (uint64_t)py * a.width + px;
         ok[j] = r < a.rows && px < a.width && gtid < a.limit;
@@ -291,15 +291,17 @@ extern "C" int ofl_mandelbrot(ofl_stream* s, uint32_t* out, uint32_t width, uint
       const double lim = 1e10;
       const bool intcmp = esc > 0.0 && esc <= lim && fabs(re0) <= lim && fabs(re1) <= lim &&
                           fabs(im0) <= lim && fabs(im1) <= lim;
-      // 4 pixels per thread in lock step, measured fastest of 1/2/3/4
-      // (profiles/r01_mandel_sweep.txt; the other forms were removed)
+      // pixels per thread in lock step: the plain kernel 4 (fastest of 1-4,
+      // profiles/r01_mandel_sweep.txt); with cycle detection 2 (a warp then
+      // waits on the slowest of 64 pixels, not 128: 1.20 vs 1.32 ms for
+      // config 3, profiles/r02_mandel_p_sweep.txt)
       if (intcmp)
         if (a.period)
-          k_mandelbrotP<true, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+          k_mandelbrotP<true, 2, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
         else
           k_mandelbrotP<true, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       else if (a.period)
-        k_mandelbrotP<false, 4, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
+        k_mandelbrotP<false, 2, true><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       else
         k_mandelbrotP<false, 4><<<(unsigned)blocks, kThreads, 0, s->cs>>>(a, queue);
       e = cudaPeekAtLastError();
