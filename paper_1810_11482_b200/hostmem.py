@@ -32,31 +32,39 @@ READ_CHUNK = 8 << 20         # D2H piece of a chunked read
 _MIN_CLASS = 4096
 
 _ranges_lock = threading.Lock()
-_starts: list[int] = []
-_ends: list[int] = []
+# (starts, ends) of the pinned allocations, sorted; replaced as a whole under
+# the lock (copy on write), so a lookup reads one consistent pair without it
+_ranges: tuple = ((), ())
 
 
 def _register_range(start: int, size: int) -> None:
+    global _ranges
     with _ranges_lock:
-        i = bisect.bisect_left(_starts, start)
-        _starts.insert(i, start)
-        _ends.insert(i, start + size)
+        starts, ends = list(_ranges[0]), list(_ranges[1])
+        i = bisect.bisect_left(starts, start)
+        starts.insert(i, start)
+        ends.insert(i, start + size)
+        _ranges = (tuple(starts), tuple(ends))
 
 
 def _unregister_range(start: int) -> None:
+    global _ranges
     with _ranges_lock:
-        i = bisect.bisect_left(_starts, start)
-        if i < len(_starts) and _starts[i] == start:
-            del _starts[i]
-            del _ends[i]
+        starts, ends = list(_ranges[0]), list(_ranges[1])
+        i = bisect.bisect_left(starts, start)
+        if i < len(starts) and starts[i] == start:
+            del starts[i]
+            del ends[i]
+            _ranges = (tuple(starts), tuple(ends))
 
 
 def is_pinned(addr: int, size: int) -> bool:
     """True if [addr, addr+size) lies inside one pinned allocation."""
-    if not _starts:
+    starts, ends = _ranges
+    if not starts:
         return False
-    i = bisect.bisect_right(_starts, addr) - 1
-    return i >= 0 and addr + size <= _ends[i]
+    i = bisect.bisect_right(starts, addr) - 1
+    return i >= 0 and addr + size <= ends[i]
 
 
 def _host_alloc(nbytes: int) -> int:
