@@ -109,6 +109,11 @@ int ofl_gate_signal(ofl_stream* s, unsigned long long* counter, uint64_t value, 
 int ofl_gate_wait(ofl_stream* s, const unsigned long long* const* counters_dev, int count,
                   uint64_t target, unsigned long long* status, uint64_t* ticket);
 int ofl_free(int dev, void* dptr);
+/* Give the device back every byte released buffers still hold: waits for the
+ * frees queued behind other streams' work, trims the pool, unmaps the cached
+ * VMM mappings (torch.cuda.empty_cache's role; an allocation that runs out
+ * does this by itself, the cheap part first). */
+int ofl_trim_memory(int dev);
 int ofl_host_alloc(uint64_t bytes, void** hptr); /* pinned, portable */
 int ofl_host_free(void* hptr);
 

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "ofl_malloc": (c_int, [c_int, c_uint64, POINTER(c_void_p)]),
     "ofl_malloc_shareable": (c_int, [c_int, c_uint64, POINTER(c_void_p)]),
     "ofl_free": (c_int, [c_int, c_void_p]),
+    "ofl_trim_memory": (c_int, [c_int]),
     "ofl_host_alloc": (c_int, [c_uint64, POINTER(c_void_p)]),
     "ofl_host_free": (c_int, [c_void_p]),
     "ofl_h2d": (c_int, [_c_stream, c_void_p, c_void_p, c_uint64, _u64p]),

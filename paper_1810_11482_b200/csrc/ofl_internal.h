@@ -71,7 +71,7 @@ int vmm_alloc(int dev, size_t bytes, void** out);
 bool vmm_owns(void* p);
 bool vmm_free_after(void* p, std::vector<cudaEvent_t>& fences);
 void vmm_drain();
-void vmm_trim(int dev);
+void vmm_trim(int dev, size_t need = 0);
 void vmm_grant_peer(int from, int to);
 // Scratch of at least `bytes` on the stream's device (caller holds s->mu).
 int stream_scratch(ofl_stream* s, size_t bytes, void** out);

@@ -393,19 +393,33 @@ static int oom(int dev, uint64_t bytes) {
                                     " bytes requested, allocation failed");
 }
 
-// hand every byte freed memory holds back to the device (before retrying an
-// allocation that ran out): frees still queued behind other streams' work,
-// the stream-ordered pool's kept blocks, released VMM mappings
-static void reclaim(int dev) {
-  {
+// Hand memory that freed buffers hold back to the device (before retrying an
+// allocation that ran out).  First without waiting for anything: the pool's
+// kept blocks and the released VMM mappings cached for reuse.  Only with
+// `wait` also the frees still queued behind other streams' work (their fence
+// events), which can take as long as those streams' kernel chains -- so an
+// allocation that the caches can satisfy never stalls behind them.
+static void reclaim(int dev, bool wait, size_t need) {
+  if (wait) {
     std::lock_guard<std::mutex> f(g_free_mu[dev]);
     if (g_free_stream[dev]) cudaStreamSynchronize(g_free_stream[dev]);
   }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-  vmm_drain();
-  vmm_trim(dev);
+  if (wait) vmm_drain();
+  // the first pass unmaps only what the request needs (largest cached
+  // mappings first); waiting frees everything
+  vmm_trim(dev, wait ? 0 : need);
   (void)cudaGetLastError();
+}
+
+int ofl_trim_memory(int dev) {
+  if (dev < 0 || dev >= kMaxDev) return set_error(OFL_ERR_BAD_ARGS, "bad device ordinal");
+  cudaError_t e = use_device(dev);
+  if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
+  std::lock_guard<std::mutex> g(g_zero_mu[dev]);
+  reclaim(dev, true, 0);
+  return OFL_OK;
 }
 
 int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
@@ -425,8 +439,8 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
     // large buffers: their own mapping (fast to create, freed without any
     // device-wide synchronisation; ofl_vmm.cu)
     int st = vmm_alloc(dev, bytes, &p);
-    if (st == OFL_ERR_OOM) {
-      reclaim(dev);
+    for (int wait = 0; st == OFL_ERR_OOM && wait < 2; ++wait) {
+      reclaim(dev, wait != 0, bytes);
       st = vmm_alloc(dev, bytes, &p);
     }
     if (st) return st;
@@ -441,9 +455,9 @@ int ofl_malloc(int dev, uint64_t bytes, void** dptr) {
     return OFL_OK;
   }
   e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
-  if (e == cudaErrorMemoryAllocation) {
+  for (int wait = 0; e == cudaErrorMemoryAllocation && wait < 2; ++wait) {
     (void)cudaGetLastError();
-    reclaim(dev);
+    reclaim(dev, wait != 0, bytes);
     e = cudaMallocAsync(&p, bytes, g_zero_stream[dev]);
   }
   if (e != cudaSuccess) {
@@ -470,9 +484,9 @@ int ofl_malloc_shareable(int dev, uint64_t bytes, void** dptr) {
   if (e != cudaSuccess) return cuda_error(e, "cudaSetDevice");
   void* p = nullptr;
   e = cudaMalloc(&p, bytes);
-  if (e == cudaErrorMemoryAllocation) {
+  for (int wait = 0; e == cudaErrorMemoryAllocation && wait < 2; ++wait) {
     (void)cudaGetLastError();
-    reclaim(dev);
+    reclaim(dev, wait != 0, bytes);
     e = cudaMalloc(&p, bytes);
   }
   if (e != cudaSuccess) {

@@ -21,6 +21,7 @@
 
 #include <condition_variable>
 #include <deque>
+#include <iterator>
 #include <map>
 #include <set>
 #include <thread>
@@ -256,14 +257,23 @@ void vmm_drain() {
   Q.idle_cv.wait(lk, [&] { return Q.q.empty() && Q.busy == 0; });
 }
 
-// unmap every cached mapping of `dev` (before retrying a failed allocation)
-void vmm_trim(int dev) {
-  std::multimap<size_t, Mapping> drop;
+// unmap cached mappings of `dev`, largest first, until `need` bytes are
+// released (0: all of them) -- before retrying a failed allocation; the
+// small ones stay cached for the allocations that reuse them
+void vmm_trim(int dev, size_t need) {
+  std::vector<Mapping> drop;
   {
     std::lock_guard<std::mutex> g(g_mu);
-    drop.swap(g_cache[dev]);
+    auto& c = g_cache[dev];
+    size_t got = 0;
+    while (!c.empty() && (need == 0 || got < need)) {
+      auto it = std::prev(c.end());
+      got += it->second.size;
+      drop.push_back(it->second);
+      c.erase(it);
+    }
   }
-  for (auto& kv : drop) unmap(kv.second);
+  for (auto& m : drop) unmap(m);
 }
 
 // `from` may now read and write `to`'s VMM buffers, current and future

@@ -289,6 +289,11 @@ class DeviceObject:
     def allocated_bytes(self) -> int:
         return self._allocated
 
+    def trim_memory(self) -> None:
+        """Return the memory released buffers still hold to the device (waits
+        for frees queued behind in-flight work; ofl_trim_memory)."""
+        _native.check(_native.load().ofl_trim_memory(self.ordinal), "trim memory")
+
     def event_log(self) -> list:
         """Traced operations (Runtime(record_events=True)); empty otherwise."""
         return self.tracer.event_log() if self.tracer is not None else []

@@ -296,6 +296,12 @@ class Runtime:
     def device_objects(self) -> list[DeviceObject]:
         return [o for _, o in self._devices]
 
+    def trim_memory(self) -> None:
+        """Return the memory that released buffers still hold (stream-ordered
+        pool blocks, cached VMM mappings) to every local device."""
+        for _, o in self._devices:
+            o.trim_memory()
+
     def local_device_object(self, gid: GlobalId) -> Optional[DeviceObject]:
         for g, o in self._devices:
             if g == gid:

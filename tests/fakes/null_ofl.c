@@ -27,6 +27,7 @@ uint64_t ofl_stream_done(void* s) { return ((S*)s)->done; }
 void* ofl_stream_handle(void* s) { return s; }
 int ofl_malloc(int d, uint64_t n, void** p) { (void)d; *p = calloc(1, n); return 0; }
 int ofl_free(int d, void* p) { (void)d; free(p); return 0; }
+int ofl_trim_memory(int d) { (void)d; return 0; }
 int ofl_malloc_shareable(int d, uint64_t n, void** p) { (void)d; *p = calloc(1, n); return 0; }
 int ofl_host_alloc(uint64_t n, void** p) { *p = calloc(1, n ? n : 1); return 0; }
 int ofl_host_free(void* p) { free(p); return 0; }

@@ -18,13 +18,17 @@ def _warm(rt, dev):
     thread, pool setup) outside the measured part, and one released buffer
     of each size the tests allocate: a first-time physical allocation may
     wait behind queued work inside the driver; steady-state allocations
-    reuse released memory and make no driver call."""
+    reuse released memory and make no driver call.  The memory earlier
+    tests released is handed back first (Runtime.trim_memory), so these
+    allocations find room without a reclaim that would empty the caches."""
+    dev.synchronize().get()
+    rt.trim_memory()
     for size in (32 << 20, 4 << 20, 4 << 20, 1 << 20, 1 << 10):
         b = dev.create_buffer(size).get()
         rt.registry.unregister(b.gid)
         del b
     dev.synchronize().get()
-    time.sleep(0.05)  # the reaper has passed their (already complete) fences
+    time.sleep(0.2)  # the reaper has passed their (already complete) fences
 
 
 def _long_heat(dev, stream: int, n: int = 1 << 27, steps: int = 6000):
@@ -76,6 +80,27 @@ def test_freed_memory_not_reused_before_prior_work(rt, dev):
         assert np.array_equal(got, pattern)
 
 
+def test_trim_memory_returns_released_memory(rt, dev):
+    """Runtime.trim_memory: released buffers' memory (cached VMM mappings,
+    pool blocks) goes back to the device."""
+    import torch
+
+    dev.synchronize().get()
+    rt.trim_memory()
+    free0, _ = torch.cuda.mem_get_info(0)
+    bufs = [dev.create_buffer(1 << 30).get() for _ in range(4)] + [dev.create_buffer(1 << 12).get()]
+    for b in bufs:
+        rt.registry.unregister(b.gid)
+    del bufs, b
+    dev.synchronize().get()
+    time.sleep(0.2)
+    held, _ = torch.cuda.mem_get_info(0)
+    assert held <= free0 - (4 << 30) + (64 << 20)   # cached for reuse, not yet returned
+    rt.trim_memory()
+    free1, _ = torch.cuda.mem_get_info(0)
+    assert free1 >= free0 - (64 << 20)
+
+
 def test_allocation_after_free_does_not_wait(rt, dev):
     """Allocations go to their own stream: they never queue behind a free's
     fence waits."""
@@ -117,3 +142,4 @@ def test_released_memory_is_reclaimed_for_other_sizes(rt, dev):
     del b
     small = dev.create_buffer(1 << 10).get()
     assert small.enqueue_read(0, 16).get() == bytes(16)
+
